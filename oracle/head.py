@@ -1,0 +1,333 @@
+"""CPU float64 oracle of the GRPO policy-loss head -- TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py (cpu_baseline leg and
+``--impl reference``) may import this module. It shares no code with the
+CUDA path. Plain NumPy float64 (OpenBLAS dgemm as the only library step),
+obviously-correct loops over rows/groups, ``math.fsum`` for scalar sums.
+
+Citations: P:Lnnn = /root/reference/PAPER.md line nnn; "reading #k" =
+DESIGN.md §3 row k (the paper is silent there).
+
+Pins (tests/test_oracle_pins.py): brute-force mpmath softmax, closed forms
+(zero logits, GRPO +-5 groups, ratio = 1, clip quadrants), invariants,
+torch float64 autograd of the definitional loss, central finite
+differences. Parity against the paper's *readings* (#5-#8, #12-#16) is
+"parity unpinned": PAPER.md prints no number that fixes them.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+# Device error-word bits ("Device validation"). Restated here
+# from the spec, not shared with include/rlhead.h.
+ERR_CU_SEQLENS = 1   # cu_seqlens[0] != 0, decreasing, or cu[S] != num_rows
+ERR_TARGET = 2       # a target id outside [0, V)
+ERR_GROUP = 4        # a group id outside [0, num_groups)
+
+_CHUNK = 512         # rows per float64 logits chunk
+
+
+# --------------------------------------------------------------------------
+# H1: packing / index bookkeeping (packed ragged batch, response mask).
+# P:L202-203 ("per response ... or at least a micro-batch of responses"),
+# BASELINE.json north_star ("packed variable-length sequences with a
+# response mask and group ids").
+# --------------------------------------------------------------------------
+def bookkeeping(cu_seqlens, mask, targets, vocab):
+    """Validate a packed batch and list its active rows.
+
+    Returns dict(row_seq int32[R], active bool[R], active_idx int32[T],
+    n_active int, err int).
+
+    * cu_seqlens must satisfy cu[0] = 0, cu[s] <= cu[s+1], cu[S] = R
+      (R = len(mask)). If not, ERR_CU_SEQLENS is raised in ``err``, every row
+      is inactive and row_seq = -1 everywhere (reading #23).
+    * row_seq[t] = the s with cu[s] <= t < cu[s+1].
+    * row t is active iff the batch is well formed, mask[t] != 0 and
+      0 <= targets[t] < V. An out-of-range target of a masked-in row raises
+      ERR_TARGET and the row becomes inactive.
+    * active_idx lists the active rows in increasing (packed) order.
+    """
+    cu = [int(x) for x in np.asarray(cu_seqlens).reshape(-1)]
+    mask = np.asarray(mask).reshape(-1)
+    targets = np.asarray(targets).reshape(-1)
+    R = mask.shape[0]
+    S = len(cu) - 1
+    err = 0
+    ok = S >= 0 and len(cu) >= 1 and cu[0] == 0 and cu[-1] == R
+    for s in range(S):
+        if cu[s] > cu[s + 1]:
+            ok = False
+    row_seq = np.full(R, -1, dtype=np.int32)
+    active = np.zeros(R, dtype=bool)
+    if not ok:
+        err |= ERR_CU_SEQLENS
+        return dict(row_seq=row_seq, active=active,
+                    active_idx=np.zeros(0, dtype=np.int32), n_active=0, err=err)
+    for s in range(S):
+        for t in range(cu[s], cu[s + 1]):
+            row_seq[t] = s
+    for t in range(R):
+        if mask[t] != 0:
+            y = int(targets[t])
+            if 0 <= y < vocab:
+                active[t] = True
+            else:
+                err |= ERR_TARGET
+    active_idx = np.array([t for t in range(R) if active[t]], dtype=np.int32)
+    return dict(row_seq=row_seq, active=active, active_idx=active_idx,
+                n_active=int(active_idx.shape[0]), err=err)
+
+
+# --------------------------------------------------------------------------
+# H3 + H4: projection z = tau^-1 W h, log-softmax at the target, entropy.
+# "computes logarithmic probabilities for these responses" (
+# reading #1: natural-log softmax over the full V at the pre-shifted target).
+# Entropy (reading #4): Shannon entropy in nats of softmax(z).
+# --------------------------------------------------------------------------
+def _as64(x):
+    """float64 copy of a numpy array or torch tensor (exact for bf16/fp32)."""
+    if hasattr(x, "detach"):
+        x = x.detach().to("cpu")
+        import torch
+        x = x.to(torch.float64).numpy()
+    return np.asarray(x, dtype=np.float64)
+
+
+def _row_softmax_stats(Hrows, W, targets_rows, inv_temperature):
+    """For a chunk of rows: z = tau^-1 H W^T; lse, logp, p, entropy."""
+    Z = (Hrows @ W.T) * inv_temperature                 # [n, V] float64
+    m = Z.max(axis=1, keepdims=True)
+    lse = (m + np.log(np.exp(Z - m).sum(axis=1, keepdims=True)))[:, 0]
+    P = np.exp(Z - lse[:, None])
+    zy = Z[np.arange(Z.shape[0]), targets_rows]
+    logp = zy - lse
+    entropy = lse - (P * Z).sum(axis=1)
+    return Z, P, lse, logp, entropy
+
+
+def logprob_fwd(hidden, weight, cu_seqlens, mask, targets, inv_temperature=1.0,
+                rows=None):
+    """Per-row log-prob / entropy / lse of the target token (fp64).
+
+    hidden [R, h], weight [V, h] (nn.Linear layout). Inactive rows (see
+    ``bookkeeping``) get 0 in all three outputs. ``rows`` restricts the work to
+    a subset of rows (sampled parity at full size); other rows are left 0.
+    Returns dict(logp, entropy, lse, err, active).
+    """
+    W = _as64(weight)
+    V = W.shape[0]
+    bk = bookkeeping(cu_seqlens, mask, targets, V)
+    R = np.asarray(mask).shape[0]
+    logp = np.zeros(R)
+    ent = np.zeros(R)
+    lse = np.zeros(R)
+    want = bk["active_idx"] if rows is None else np.array(
+        [t for t in np.asarray(rows).reshape(-1) if bk["active"][t]], dtype=np.int64)
+    targets = np.asarray(targets).reshape(-1)
+    for c0 in range(0, len(want), _CHUNK):
+        idx = want[c0:c0 + _CHUNK]
+        Hc = _as64(_take_rows(hidden, idx))
+        _, _, l, lp, e = _row_softmax_stats(Hc, W, targets[idx].astype(np.int64), inv_temperature)
+        logp[idx], ent[idx], lse[idx] = lp, e, l
+    return dict(logp=logp, entropy=ent, lse=lse, err=bk["err"], active=bk["active"])
+
+
+def _take_rows(x, idx):
+    """Rows ``idx`` of a numpy array or torch tensor (any device)."""
+    idx = np.asarray(idx, dtype=np.int64)
+    if hasattr(x, "detach"):
+        import torch
+        return x[torch.as_tensor(idx, device=x.device)]
+    return np.asarray(x)[idx]
+
+
+# --------------------------------------------------------------------------
+# H2: GRPO group-relative advantage.
+# GRPO generates G responses per query; "normalization must
+# aggregate all responses for a query"; rewards +-5.
+# Formula (reading #5): A_i = (r_i - mu_g) / (sigma_g + eps) within the group,
+# sigma unbiased (n-1) by default (reading #6), eps = 1e-6 (reading #7),
+# A = 0 exactly when n_g = 1 or max_g r = min_g r (reading #8).
+# --------------------------------------------------------------------------
+def grpo_group_stats(rewards, group_of_seq, num_groups):
+    """Per-group sufficient statistics of the rewards.
+
+    sum_stats[g] = (n_g, sum r, sum r^2) and max_stats[g] = (max r, -min r),
+    over the sequences with a valid group id (others raise ERR_GROUP). Groups
+    with no member: (0, 0, 0) and (-inf, -inf).
+    """
+    r = _as64(rewards).reshape(-1)
+    gos = np.asarray(group_of_seq).reshape(-1)
+    sum_stats = np.zeros((num_groups, 3))
+    max_stats = np.full((num_groups, 2), -np.inf)
+    err = 0
+    members = [[] for _ in range(num_groups)]
+    for i in range(r.shape[0]):
+        g = int(gos[i])
+        if 0 <= g < num_groups:
+            members[g].append(float(r[i]))
+        else:
+            err |= ERR_GROUP
+    for g in range(num_groups):
+        xs = members[g]
+        if xs:
+            sum_stats[g] = (len(xs), math.fsum(xs), math.fsum(x * x for x in xs))
+            max_stats[g] = (max(xs), -min(xs))
+    return sum_stats, max_stats, err
+
+
+def grpo_advantage(rewards, group_of_seq, num_groups, eps=1e-6, unbiased=True):
+    """A_i per sequence, the plain two-pass definition (mean, then squared
+    deviations). Sequences with an invalid group id get A = 0 and ERR_GROUP."""
+    r = _as64(rewards).reshape(-1)
+    gos = np.asarray(group_of_seq).reshape(-1)
+    adv = np.zeros(r.shape[0])
+    err = 0
+    for i in range(r.shape[0]):
+        if not (0 <= int(gos[i]) < num_groups):
+            err |= ERR_GROUP
+    for g in range(num_groups):
+        idx = [i for i in range(r.shape[0]) if int(gos[i]) == g]
+        n = len(idx)
+        if n == 0:
+            continue
+        xs = [float(r[i]) for i in idx]
+        if n == 1 or max(xs) == min(xs):
+            continue                       # A = 0 exactly (reading #8)
+        mu = math.fsum(xs) / n
+        var = math.fsum((x - mu) ** 2 for x in xs) / ((n - 1) if unbiased else n)
+        sigma = math.sqrt(var)
+        for i, x in zip(idx, xs):
+            adv[i] = (x - mu) / (sigma + eps)
+    return adv, err
+
+
+def grpo_advantage_from_stats(rewards, group_of_seq, sum_stats, max_stats, eps=1e-6,
+                              unbiased=True):
+    """A_i from (possibly all-reduced) group statistics: the split-group form
+    (a group's responses on several DP ranks).
+    mu = S1/n, var = (S2 - n mu^2) / (n - 1 | n); A = 0 if n <= 1 or max = min."""
+    r = _as64(rewards).reshape(-1)
+    gos = np.asarray(group_of_seq).reshape(-1)
+    G = np.asarray(sum_stats).shape[0]
+    adv = np.zeros(r.shape[0])
+    for i in range(r.shape[0]):
+        g = int(gos[i])
+        if not (0 <= g < G):
+            continue
+        n, s1, s2 = (float(v) for v in sum_stats[g])
+        mx, negmn = float(max_stats[g][0]), float(max_stats[g][1])
+        if n <= 1 or mx == -negmn:
+            continue
+        mu = s1 / n
+        var = max(s2 - n * mu * mu, 0.0) / ((n - 1) if unbiased else n)
+        adv[i] = (float(r[i]) - mu) / (math.sqrt(var) + eps)
+    return adv
+
+
+# --------------------------------------------------------------------------
+# H5: ratio, clipped surrogate, token-level mean; H6-H8: backward.
+# "Token-Level Loss: ... compute the average over tokens, as in DAPO";
+# "discard minibatches with too large importance ratio" (P:L830 -> ratio
+# statistics are emitted). Surrogate (readings #12-#15):
+#   d = logp - old, r = exp(clamp(d, -c, c)),
+#   l = max(-A r, -A clip(r, 1-eps_lo, 1+eps_hi)),  L = sum_t m_t l_t / N,
+#   dL/dlogp = -(m/N) A r * act * [|d| <= c],
+#   act = not((A > 0 and r > 1+eps_hi) or (A < 0 and r < 1-eps_lo)).
+# Backward through softmax: dz = tau^-1 g (onehot(y) - p); dH = dz W;
+# dW = sum_t dz_t^T h_t (BASELINE.json north_star: "dL/dhidden and dL/dW").
+# --------------------------------------------------------------------------
+@dataclass
+class LossParams:
+    clip_lo: float = 0.2
+    clip_hi: float = 0.2
+    logratio_clamp: float = 20.0
+    loss_scale: float | None = None     # None -> 1 / n_global
+
+
+def _surrogate(logp, old, A, p: LossParams):
+    d = logp - old
+    c = p.logratio_clamp
+    r = math.exp(min(max(d, -c), c))
+    lo, hi = 1.0 - p.clip_lo, 1.0 + p.clip_hi
+    rc = min(max(r, lo), hi)
+    loss = max(-A * r, -A * rc)
+    clipped_hi = A > 0 and r > hi
+    clipped_lo = A < 0 and r < lo
+    act = not (clipped_hi or clipped_lo)
+    inrange = abs(d) <= c
+    dl_dlogp = (-A * r) if (act and inrange) else 0.0
+    return r, loss, dl_dlogp, clipped_lo, clipped_hi
+
+
+def policy_loss_fwd_bwd(hidden, weight, cu_seqlens, mask, targets, old_logp, adv_seq,
+                        params: LossParams | None = None, n_global=None,
+                        inv_temperature=1.0, want_grads=True):
+    """Forward + backward of the masked clipped-ratio token-mean loss.
+
+    hidden [R, h]; weight [V, h]; old_logp [R]; adv_seq [S] (one advantage per
+    sequence, broadcast to its rows). n_global = the loss normaliser N (masked
+    tokens of the whole mini-batch over all ranks, reading #13); defaults to
+    this batch's active count. loss_scale, when given, replaces 1/N.
+
+    Returns dict(loss, loss_sum, logp, entropy, lse, g, dH [R,h], dW [V,h],
+    stats{loss_sum, ratio_sum, entropy_sum, ratio_max, clip_lo_count,
+    clip_hi_count, tokens}, err). Inactive rows: logp = entropy = lse = g = 0
+    and dH row = 0.
+    """
+    p = params or LossParams()
+    W = _as64(weight)
+    V, h = W.shape
+    bk = bookkeeping(cu_seqlens, mask, targets, V)
+    R = np.asarray(mask).shape[0]
+    targets = np.asarray(targets).reshape(-1).astype(np.int64)
+    old = _as64(old_logp).reshape(-1)
+    adv = _as64(adv_seq).reshape(-1)
+    N = bk["n_active"] if n_global is None else int(n_global)
+    scale = (1.0 / N if N > 0 else 0.0) if p.loss_scale is None else float(p.loss_scale)
+
+    logp = np.zeros(R)
+    ent = np.zeros(R)
+    lse = np.zeros(R)
+    g = np.zeros(R)
+    dH = np.zeros((R, h)) if want_grads else None
+    dW = np.zeros((V, h)) if want_grads else None
+    losses, ratios, ents = [], [], []
+    ratio_max = 0.0
+    n_lo = n_hi = 0
+    act_rows = bk["active_idx"].astype(np.int64)
+    for c0 in range(0, len(act_rows), _CHUNK):
+        idx = act_rows[c0:c0 + _CHUNK]
+        Hc = _as64(_take_rows(hidden, idx))
+        Z, P, l, lp, e = _row_softmax_stats(Hc, W, targets[idx], inv_temperature)
+        logp[idx], ent[idx], lse[idx] = lp, e, l
+        gc = np.zeros(len(idx))
+        for j, t in enumerate(idx):
+            A = float(adv[bk["row_seq"][t]])
+            r, loss, dldlp, clo, chi = _surrogate(float(lp[j]), float(old[t]), A, p)
+            losses.append(loss)
+            ratios.append(r)
+            ents.append(float(e[j]))
+            ratio_max = max(ratio_max, r)
+            n_lo += int(clo)
+            n_hi += int(chi)
+            gc[j] = scale * dldlp
+        g[idx] = gc
+        if want_grads:
+            onehot = np.zeros_like(P)
+            onehot[np.arange(len(idx)), targets[idx]] = 1.0
+            dZ = inv_temperature * gc[:, None] * (onehot - P)
+            dH[idx] = dZ @ W
+            dW += dZ.T @ Hc
+    loss_sum = math.fsum(losses)
+    stats = dict(loss_sum=loss_sum, ratio_sum=math.fsum(ratios), entropy_sum=math.fsum(ents),
+                 ratio_max=ratio_max, clip_lo_count=n_lo, clip_hi_count=n_hi,
+                 tokens=len(act_rows))
+    loss = loss_sum * scale
+    return dict(loss=loss, loss_sum=loss_sum, logp=logp, entropy=ent, lse=lse, g=g,
+                dH=dH, dW=dW, stats=stats, err=bk["err"], active=bk["active"],
+                row_seq=bk["row_seq"], n_active=bk["n_active"])

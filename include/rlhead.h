@@ -1,0 +1,204 @@
+/*
+ * rlhead.h -- C ABI of the B200 (sm_100a) GRPO policy-loss head.
+ *
+ * The token-level policy-loss head that RLinf's inference worker (old/ref
+ * log-probs) and training worker (policy update,
+ * P:L181) run on every micro-batch: LM-head projection
+ * Z = tau^-1 H W^T, online log-sum-exp over the vocabulary, target gather
+ * (log-prob, entropy), GRPO group-relative advantages (P:L178-179,
+ * P:L388-391), the masked clipped-ratio surrogate with token-level averaging
+ * and its backward dL/dH, dL/dW. Formulas: DESIGN.md §2 (O.1);
+ * readings of what the paper leaves open: DESIGN.md §3.
+ *
+ * Conventions for every call:
+ *   - Pointers are DEVICE pointers unless the comment says "host".
+ *   - Calls are asynchronous and stream-ordered on `stream` (a cudaStream_t;
+ *     NULL = legacy default stream). No call allocates device memory,
+ *     synchronises the stream or keeps state between calls; all scratch lives
+ *     in the caller's workspace `ws` (size from rl_workspace_size).
+ *   - The caller owns every buffer. Outputs are overwritten unless marked
+ *     "accumulated (+=)".
+ *   - Host-side argument errors return RL_ERR_* with NOTHING launched.
+ *   - Data errors found on the device (bad cu_seqlens, target or group id)
+ *     are OR-ed into the optional device word `err_flags` (RL_DEVERR_*) and
+ *     the offending rows/sequences are treated as inactive; no host sync.
+ *   - Re-entrant: concurrent calls on different streams are legal when their
+ *     outputs and workspaces are disjoint.
+ */
+#ifndef RLHEAD_H
+#define RLHEAD_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define RL_API __attribute__((visibility("default")))
+#else
+#define RL_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *rl_stream_t; /* == cudaStream_t */
+
+typedef enum {
+  RL_OK = 0,
+  RL_ERR_INVALID_ARG = 1, /* null/negative/misaligned argument, nothing launched */
+  RL_ERR_UNSUPPORTED = 2, /* valid but unsupported shape/dtype on this build/device */
+  RL_ERR_WORKSPACE = 3,   /* ws NULL or ws_bytes < rl_workspace_size(...) */
+  RL_ERR_CUDA = 4         /* a CUDA runtime/driver call failed */
+} rl_status;
+
+typedef enum { RL_F32 = 0, RL_BF16 = 1 } rl_dtype;
+
+/* Device error word bits (err_flags). */
+#define RL_DEVERR_CU_SEQLENS 1 /* cu[0]!=0, decreasing, or cu[S]!=num_rows: ALL rows inactive */
+#define RL_DEVERR_TARGET 2     /* mask!=0 row with target outside [0,V): that row inactive */
+#define RL_DEVERR_GROUP 4      /* group id outside [0,num_groups): that sequence gets A=0 */
+
+/* Packed ragged micro-batch (BASELINE.json north_star: "packed variable-
+ * length sequences with a response mask and group ids").
+ * Row t belongs to sequence s iff cu_seqlens[s] <= t < cu_seqlens[s+1].
+ * Row t is ACTIVE iff the batch is well formed, mask[t] != 0 and
+ * 0 <= targets[t] < vocab. Active rows are processed in packed order. */
+typedef struct {
+  int64_t num_rows;          /* R >= 0: packed rows incl. prompt rows          */
+  int32_t num_seqs;          /* S >= 0                                          */
+  const int32_t *cu_seqlens; /* [S+1]                                           */
+  const int32_t *targets;    /* [R] token id predicted by row t (pre-shifted)   */
+  const uint8_t *mask;       /* [R] != 0: response token that carries the loss  */
+  int32_t *err_flags;        /* optional device int32, RL_DEVERR_* OR-ed in     */
+} rl_batch;
+
+/* The LM head (host struct). hidden is [num_rows, ld_hidden] row-major of
+ * `dtype`; weight is W[vocab, hidden] row-major (nn.Linear layout), same
+ * dtype, densely packed (row stride = hidden). logits = inv_temperature*H W^T.
+ * RL_BF16 runs the tcgen05/TMEM/TMA tensor-core path and needs hidden % 64
+ * == 0 and ld_hidden % 8 == 0; RL_F32 runs the exact-fp32 CUDA-core path. */
+typedef struct {
+  int32_t hidden;        /* h  (1..65536)                                      */
+  int32_t vocab;         /* V  (1..2^24)                                       */
+  rl_dtype dtype;        /* RL_F32 | RL_BF16                                   */
+  int64_t ld_hidden;     /* row stride of hidden / grad_hidden in elements >= h */
+  float inv_temperature; /* tau^-1 > 0 (1 = plain softmax)                     */
+} rl_head;
+
+/* Workspace bytes for a call on up to `num_rows` packed rows;
+ * want_bwd != 0 for rl_policy_loss_fwd_bwd. 0 if the head is invalid. */
+RL_API size_t rl_workspace_size(const rl_head *hd, int64_t num_rows, int32_t want_bwd);
+
+/* H1 bookkeeping alone (it also runs inside the two head calls).
+ * row_seq [R] (out, may be NULL): sequence of row t, -1 on a malformed batch.
+ * active_idx [R] (out, may be NULL): active rows in packed order; entries
+ *   at and beyond n_active are left unspecified.
+ * n_active (device int64, out, may be NULL): number of active rows.
+ * n_accum (device int64, ACCUMULATED +=, may be NULL): for the loss
+ *   normaliser N summed over micro-batches/ranks (DESIGN.md §3 #13). */
+RL_API rl_status rl_batch_prepare(const rl_head *hd, const rl_batch *b, int32_t *row_seq,
+                           int32_t *active_idx, int64_t *n_active, int64_t *n_accum,
+                           void *ws, size_t ws_bytes, rl_stream_t stream);
+
+/* Inference-worker call: per-row log-prob of the
+ * target, entropy (nats) and log-sum-exp of tau^-1 H W^T over the full V.
+ * logp/entropy/lse are [R] fp32 (entropy, lse may be NULL); 0 on inactive
+ * rows. Full logits never reach HBM. */
+RL_API rl_status rl_logprob_fwd(const rl_head *hd, const void *hidden, const void *weight,
+                         const rl_batch *b, float *logp, float *entropy, float *lse,
+                         void *ws, size_t ws_bytes, rl_stream_t stream);
+
+/* GRPO group statistics (normalisation aggregates all responses
+ * of a query). Over sequences with a valid group id:
+ *   sum_stats[g] = (n_g, sum r, sum r^2)   fp64 [num_groups][3], out
+ *   max_stats[g] = (max r, -min r)         fp64 [num_groups][2], out
+ * Empty groups give (0,0,0) and (-inf,-inf). Split groups across DP ranks
+ * all-reduce these (SUM / MAX) before rl_grpo_advantage. */
+RL_API rl_status rl_grpo_group_stats(const float *rewards, const int32_t *group_of_seq,
+                              int32_t num_seqs, int32_t num_groups, double *sum_stats,
+                              double *max_stats, int32_t *err_flags, rl_stream_t stream);
+
+/* GRPO advantage per sequence (formula DESIGN.md §3 #5-#8):
+ *   A_s = (r_s - mu_g) / (sigma_g + eps),  sigma over n-1 (unbiased != 0) or n,
+ *   A_s = 0 exactly when n_g <= 1 or max_g r == min_g r, or the group id is
+ *   invalid (RL_DEVERR_GROUP).
+ * sum_stats/max_stats: NULL = compute the group statistics from this call's
+ * rewards (all members local); else use the given (all-reduced) ones.
+ * adv [num_seqs] fp32 out. */
+RL_API rl_status rl_grpo_advantage(const float *rewards, const int32_t *group_of_seq,
+                            int32_t num_seqs, int32_t num_groups, const double *sum_stats,
+                            const double *max_stats, float eps, int32_t unbiased, float *adv,
+                            int32_t *err_flags, rl_stream_t stream);
+
+/* Clipped surrogate parameters (host struct; DESIGN.md §3 #12-#15). */
+typedef struct {
+  float clip_lo;                  /* eps_lo: ratio clipped below at 1 - eps_lo (0.2) */
+  float clip_hi;                  /* eps_hi: ratio clipped above at 1 + eps_hi (0.2) */
+  float logratio_clamp;           /* c: d = logp - old clamped to [-c, c] (20)       */
+  double loss_scale;              /* multiplies dL/dlogp when n_tokens_global NULL   */
+  const int64_t *n_tokens_global; /* device: N (all micro-batches, all ranks);
+                                     scale = 1/N (0 if N == 0)                      */
+} rl_loss_params;
+
+/* Loss statistics, device resident, ACCUMULATED (+=) by every call. The
+ * caller zeroes it at the start of a mini-batch. Raw sums over active rows:
+ * L = loss_sum * scale. clip_hi_count = #{A>0, r>1+eps_hi},
+ * clip_lo_count = #{A<0, r<1-eps_lo}; ratio_max feeds the minibatch
+ * early-stop. */
+typedef struct {
+  double loss_sum;
+  double ratio_sum;
+  double entropy_sum;
+  float ratio_max;
+  int32_t reserved;
+  int64_t clip_lo_count;
+  int64_t clip_hi_count;
+  int64_t tokens;
+} rl_loss_stats;
+
+/* Training-worker call: forward + backward of the masked clipped-ratio
+ * token-mean loss on one micro-batch (micro-batch = fwd/bwd unit).
+ *   old_logp [R] fp32, adv [S] fp32 (one per sequence, broadcast to its rows),
+ *   logp [R] / entropy [R] fp32 out (entropy may be NULL), 0 on inactive rows,
+ *   grad_hidden [R, ld_hidden] out, dtype of hidden, 0 on inactive rows,
+ *   grad_weight [V, h] fp32 ACCUMULATED (+=): zero it once per mini-batch,
+ *   stats (device, may be NULL) ACCUMULATED.
+ * dL/dlogp_t = -scale * A r [unclipped] [|d| <= c]; dZ = tau^-1 g (onehot-p);
+ * dH = dZ W; dW += dZ^T H. Logits are recomputed in the backward instead of
+ * stored. */
+RL_API rl_status rl_policy_loss_fwd_bwd(const rl_head *hd, const void *hidden, const void *weight,
+                                 const rl_batch *b, const float *old_logp, const float *adv,
+                                 const rl_loss_params *p, float *logp, float *entropy,
+                                 void *grad_hidden, float *grad_weight, rl_loss_stats *stats,
+                                 void *ws, size_t ws_bytes, rl_stream_t stream);
+
+/* ---- introspection / tracing (P:L682-690 worker timers, device-side) ---- */
+RL_API const char *rl_status_string(rl_status s);
+RL_API const char *rl_build_info(void);
+/* Number of kernels this library has launched since it was loaded. */
+RL_API int64_t rl_launch_count(void);
+
+/* Kernel kinds reported by the tracer. */
+typedef enum {
+  RL_K_PREPARE = 0, RL_K_GATHER = 1, RL_K_GEMM_LSE = 2, RL_K_MERGE = 3,
+  RL_K_GEMM_DZ = 4, RL_K_GEMM_DH = 5, RL_K_GEMM_DW = 6, RL_K_GRPO = 7,
+  RL_K_SIMT_FWD = 8, RL_K_SIMT_BWD = 9, RL_K_REDUCE = 10, RL_K_MISC = 11,
+  RL_K_NUM_KINDS = 12
+} rl_kernel_kind;
+
+/* Tracing (not thread-safe; for benchmarks, cf. the worker-group timers of
+ * P:L682-690). While active, every launch is bracketed by cudaEventRecord on
+ * its own stream (events owned by the library, created on first use).
+ * rl_trace_end stops tracing, writes the kind of each traced launch into
+ * kinds[0..n) (host, may be NULL) and returns n. rl_trace_durations then
+ * waits for those events and writes each launch's device time in ms
+ * (host array, up to cap entries). Launches beyond capacity_launches are
+ * counted by rl_launch_count but not traced. */
+RL_API rl_status rl_trace_begin(int32_t capacity_launches);
+RL_API int32_t rl_trace_end(int32_t *kinds);
+RL_API int32_t rl_trace_durations(float *ms, int32_t cap);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RLHEAD_H */

@@ -1,0 +1,13 @@
+"""B200-native (sm_100a) GRPO policy-loss head -- the data-parallel hot path of
+RLinf's inference and training workers (arXiv 2509.15965).
+
+The compute lives in ``librlhead.so`` (CUDA, include/rlhead.h); this package is
+its thin ctypes binding (``rlhead``) plus the host-side data-parallel driver
+(``dp``: micro-batch packing, LPT sharding, NCCL collectives).
+"""
+from .rlhead import (  # noqa: F401
+    Batch, Head, LossParams, Trace, Workspace, RLHeadError, new_stats, read_stats,
+    rl_batch_prepare, rl_build_info, rl_grpo_advantage, rl_grpo_group_stats,
+    rl_launch_count, rl_logprob_fwd, rl_policy_loss_fwd_bwd, rl_workspace_size,
+    RL_DEVERR_CU_SEQLENS, RL_DEVERR_GROUP, RL_DEVERR_TARGET, KERNEL_KINDS, EXPORTED,
+)

@@ -1,0 +1,77 @@
+// Shared host/device plumbing of librlhead: launch tracing, workspace layout,
+// small device reductions. Nothing here is numerics of the method.
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <cstdint>
+#include <cstddef>
+
+#include "../../include/rlhead.h"
+
+namespace rlh {
+
+// ---------------------------------------------------------------- tracing ----
+// Every kernel launch goes through TraceScope so that rl_launch_count() and the
+// optional event tracer (rl_trace_begin/end) see it.
+void trace_before(int kind, cudaStream_t s);
+void trace_after(int kind, cudaStream_t s);
+struct TraceScope {
+  int kind;
+  cudaStream_t s;
+  TraceScope(int k, cudaStream_t st) : kind(k), s(st) { trace_before(kind, s); }
+  ~TraceScope() { trace_after(kind, s); }
+};
+
+#define RLH_CHECK_LAUNCH()                                   \
+  do {                                                       \
+    cudaError_t e_ = cudaGetLastError();                     \
+    if (e_ != cudaSuccess) return RL_ERR_CUDA;               \
+  } while (0)
+
+// ---------------------------------------------------------------- tiling ----
+constexpr int TC_BM = 128;   // rows per tcgen05 tile (UMMA M)
+constexpr int TC_BN = 256;   // columns per tile (UMMA N)
+constexpr int TC_BK = 64;    // K per pipeline stage (one 128-B swizzle row)
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
+
+// Workspace carve-up. All offsets 256-B aligned. Sizes depend on the head,
+// the row bound R and whether the backward runs.
+struct WsLayout {
+  int64_t R, Rp;          // rows, rows padded to TC_BM (+1 tile of slack)
+  int64_t n_vt;           // vocab tiles (partials per row)
+  int64_t Vp;             // vocab padded to TC_BN (dZ row stride)
+  int64_t nblk_rows;      // 1024-row blocks of the bookkeeping kernels
+  int64_t nblk_loss;      // 256-row blocks of the merge/loss kernel
+  size_t off_hdr, off_flags, off_blkcnt, off_blkoff, off_active, off_rowseq, off_tgt,
+      off_seq, off_hc, off_pm, off_ps, off_pu, off_zy, off_lse, off_g, off_dz, off_st_d,
+      off_st_f, off_st_i, total;
+};
+bool ws_layout(const rl_head* hd, int64_t R, int want_bwd, WsLayout* L);
+
+// Header words at ws + off_hdr.
+struct WsHeader {
+  int64_t n_active;   // active rows of this call
+  int32_t bad_cu;     // malformed cu_seqlens
+  int32_t pad;
+};
+
+// ------------------------------------------------------ device reductions ----
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+template <typename T>
+__device__ __forceinline__ T warp_max(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    T w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = w > v ? w : v;
+  }
+  return v;
+}
+
+}  // namespace rlh

@@ -1,0 +1,62 @@
+// Internal launchers of librlhead (host side). Each returns RL_OK or
+// RL_ERR_CUDA and launches through TraceScope.
+#pragma once
+#include "common.cuh"
+
+namespace rlh {
+
+// H1 bookkeeping: validate cu_seqlens, per-row flags/row_seq, block scan,
+// compaction into active_idx/tgt_c/seq_c (all in ws unless user pointers
+// given). Zeroes zero0..2 [R] (fp32, may be NULL) on inactive rows.
+rl_status launch_prepare(const rl_head* hd, const rl_batch* b, const WsLayout& L, char* ws,
+                         int32_t* row_seq_user, int32_t* active_idx_user, int64_t* n_active_user,
+                         int64_t* n_accum, float* zero0, float* zero1, float* zero2,
+                         cudaStream_t s);
+// Compact bf16 rows Hc[r] = hidden[active_idx[r]], zero rows up to the tile.
+rl_status launch_gather_bf16(const rl_head* hd, const void* hidden, const WsLayout& L, char* ws,
+                             cudaStream_t s);
+// grad_hidden rows of inactive rows := 0.
+rl_status launch_zero_inactive(const rl_head* hd, void* grad_hidden, const WsLayout& L, char* ws,
+                               cudaStream_t s);
+
+// H2 GRPO.
+rl_status launch_grpo(const float* rewards, const int32_t* gos, int32_t S, int32_t G,
+                      const double* sum_in, const double* max_in, float eps, int32_t unbiased,
+                      float* adv, double* sum_out, double* max_out, int32_t* err,
+                      cudaStream_t s);
+
+// H4 merge of the split-V partials (+ H5 loss when old_logp != NULL).
+struct MergeArgs {
+  const float *pm, *ps, *pu, *zy;
+  const int32_t *active_idx, *seq_c;
+  float *logp, *entropy, *lse;          // row space, may be NULL
+  // loss
+  const float* old_logp;                // row space; NULL = fwd only
+  const float* adv;                     // per sequence
+  float clip_lo, clip_hi, clamp_c;
+  double loss_scale;
+  const int64_t* n_global;
+  float *g_c, *lse_c;                   // compact, for the backward
+  double* st_d;                         // [nblk][3] loss, ratio, entropy sums
+  float* st_f;                          // [nblk] ratio max
+  long long* st_i;                      // [nblk][3] clip_lo, clip_hi, tokens
+};
+rl_status launch_merge(const WsLayout& L, char* ws, const MergeArgs& a, cudaStream_t s);
+rl_status launch_stats_reduce(const WsLayout& L, char* ws, rl_loss_stats* stats, cudaStream_t s);
+
+// CUDA-core path (fp32 exact; also bf16 for cross-checks).
+rl_status launch_simt_fwd(const rl_head* hd, const void* hidden, const void* weight,
+                          const WsLayout& L, char* ws, cudaStream_t s);
+rl_status launch_simt_bwd(const rl_head* hd, const void* hidden, const void* weight,
+                          void* grad_hidden, float* grad_weight, const WsLayout& L, char* ws,
+                          cudaStream_t s);
+
+// Tensor-core path (bf16, tcgen05/TMEM/TMA).
+rl_status launch_tc_fwd(const rl_head* hd, const void* weight, const WsLayout& L, char* ws,
+                        cudaStream_t s);
+rl_status launch_tc_bwd(const rl_head* hd, const void* weight, void* grad_hidden,
+                        float* grad_weight, const WsLayout& L, char* ws, cudaStream_t s);
+
+int num_sms();
+
+}  // namespace rlh

@@ -1,0 +1,175 @@
+// H4 merge + H5 loss head. One thread per active (compact) row:
+//  * merge the split-V partials (m_n, s_n = sum e^{z-m_n}, u_n = sum
+//    e^{z-m_n}(z-m_n)) into lse = M + log S and entropy = log S - U/S
+//    (entropy in the shifted form avoids cancelling M), logp = z_y - lse;
+//  * H5 (P:L828 token-level mean, readings DESIGN.md §3 #12-#15):
+//    d = logp - old, r = exp(clamp(d)), l = max(-A r, -A clip(r)),
+//    g = dL/dlogp = -scale * A r [unclipped] [|d| <= c];
+//  * per-block fixed-order reduction of the loss statistics (deterministic),
+//    summed by a one-block kernel into the caller's accumulators.
+#include "kernels.h"
+
+namespace rlh {
+
+constexpr int MERGE_THREADS = 256;
+
+struct LStat {
+  double loss, ratio, ent;
+  float rmax;
+  long long clo, chi, tok;
+};
+
+__device__ __forceinline__ void lstat_add(LStat& a, const LStat& b) {
+  a.loss += b.loss;
+  a.ratio += b.ratio;
+  a.ent += b.ent;
+  a.rmax = fmaxf(a.rmax, b.rmax);
+  a.clo += b.clo;
+  a.chi += b.chi;
+  a.tok += b.tok;
+}
+
+__device__ __forceinline__ LStat lstat_shfl(const LStat& v, int o) {
+  LStat w;
+  w.loss = __shfl_xor_sync(0xffffffffu, v.loss, o);
+  w.ratio = __shfl_xor_sync(0xffffffffu, v.ratio, o);
+  w.ent = __shfl_xor_sync(0xffffffffu, v.ent, o);
+  w.rmax = __shfl_xor_sync(0xffffffffu, v.rmax, o);
+  w.clo = __shfl_xor_sync(0xffffffffu, v.clo, o);
+  w.chi = __shfl_xor_sync(0xffffffffu, v.chi, o);
+  w.tok = __shfl_xor_sync(0xffffffffu, v.tok, o);
+  return w;
+}
+
+template <int NT>
+__device__ LStat block_reduce_lstat(LStat v) {
+  __shared__ LStat sh[NT / 32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    LStat w = lstat_shfl(v, o);
+    lstat_add(v, w);
+  }
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  LStat t = sh[0];
+  for (int w = 1; w < NT / 32; ++w) lstat_add(t, sh[w]);
+  return t;
+}
+
+template <bool LOSS>
+__global__ void __launch_bounds__(MERGE_THREADS)
+k_merge(MergeArgs a, const WsHeader* __restrict__ hdr, int64_t n_vt, int64_t ldp) {
+  const int64_t T = hdr->n_active;
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * MERGE_THREADS + threadIdx.x;
+  LStat st{0.0, 0.0, 0.0, 0.f, 0, 0, 0};
+  if (r < T) {
+    float M = a.pm[r], S = a.ps[r], U = a.pu[r];
+    for (int64_t n = 1; n < n_vt; ++n) {
+      const float m = a.pm[n * ldp + r], s = a.ps[n * ldp + r], u = a.pu[n * ldp + r];
+      if (m > M) {  // rescale the running sums to the new max
+        const float f = expf(M - m);
+        U = f * (U + (M - m) * S);
+        S = f * S;
+        M = m;
+      }
+      const float f2 = expf(m - M);
+      S += s * f2;
+      U += f2 * (u + (m - M) * s);
+    }
+    const float logS = logf(S);
+    const float lse = M + logS;
+    const float ent = logS - U / S;
+    const float lp = a.zy[r] - lse;
+    const int32_t t = a.active_idx[r];
+    if (a.logp) a.logp[t] = lp;
+    if (a.entropy) a.entropy[t] = ent;
+    if (a.lse) a.lse[t] = lse;
+    if constexpr (LOSS) {
+      double scale = a.loss_scale;
+      if (a.n_global) {
+        const long long N = *a.n_global;
+        scale = N > 0 ? 1.0 / static_cast<double>(N) : 0.0;
+      }
+      const float A = a.adv[a.seq_c[r]];
+      const float d = lp - a.old_logp[t];
+      const float dc = fminf(fmaxf(d, -a.clamp_c), a.clamp_c);
+      const float ratio = expf(dc);
+      const float lo = 1.f - a.clip_lo, hi = 1.f + a.clip_hi;
+      const float rc = fminf(fmaxf(ratio, lo), hi);
+      const float loss = fmaxf(-A * ratio, -A * rc);
+      const bool chi = (A > 0.f) && (ratio > hi);
+      const bool clo = (A < 0.f) && (ratio < lo);
+      const bool flows = !(chi || clo) && (fabsf(d) <= a.clamp_c);
+      const float g = flows ? static_cast<float>(-scale * static_cast<double>(A) * ratio) : 0.f;
+      a.g_c[r] = g;
+      a.lse_c[r] = lse;
+      st = {static_cast<double>(loss), static_cast<double>(ratio), static_cast<double>(ent),
+            ratio, clo ? 1ll : 0ll, chi ? 1ll : 0ll, 1ll};
+    }
+  } else if (r < ldp) {
+    if constexpr (LOSS) {  // padding rows of the last tile: zero gradient coefficient
+      a.g_c[r] = 0.f;
+      a.lse_c[r] = 0.f;
+    }
+  }
+  if constexpr (LOSS) {
+    st = block_reduce_lstat<MERGE_THREADS>(st);
+    if (threadIdx.x == 0) {
+      a.st_d[3 * blockIdx.x] = st.loss;
+      a.st_d[3 * blockIdx.x + 1] = st.ratio;
+      a.st_d[3 * blockIdx.x + 2] = st.ent;
+      a.st_f[blockIdx.x] = st.rmax;
+      a.st_i[3 * blockIdx.x] = st.clo;
+      a.st_i[3 * blockIdx.x + 1] = st.chi;
+      a.st_i[3 * blockIdx.x + 2] = st.tok;
+    }
+  }
+}
+
+rl_status launch_merge(const WsLayout& L, char* ws, const MergeArgs& a, cudaStream_t s) {
+  const WsHeader* hdr = reinterpret_cast<const WsHeader*>(ws + L.off_hdr);
+  if (L.nblk_loss == 0) return RL_OK;
+  TraceScope ts(RL_K_MERGE, s);
+  if (a.old_logp)
+    k_merge<true><<<static_cast<unsigned>(L.nblk_loss), MERGE_THREADS, 0, s>>>(a, hdr, L.n_vt,
+                                                                                L.Rp);
+  else
+    k_merge<false><<<static_cast<unsigned>(L.nblk_loss), MERGE_THREADS, 0, s>>>(a, hdr, L.n_vt,
+                                                                                 L.Rp);
+  RLH_CHECK_LAUNCH();
+  return RL_OK;
+}
+
+__global__ void __launch_bounds__(MERGE_THREADS)
+k_stats_reduce(const double* __restrict__ st_d, const float* __restrict__ st_f,
+               const long long* __restrict__ st_i, int64_t nblk, rl_loss_stats* out) {
+  LStat v{0.0, 0.0, 0.0, 0.f, 0, 0, 0};
+  for (int64_t b = threadIdx.x; b < nblk; b += MERGE_THREADS) {
+    LStat w{st_d[3 * b], st_d[3 * b + 1], st_d[3 * b + 2], st_f[b], st_i[3 * b], st_i[3 * b + 1],
+            st_i[3 * b + 2]};
+    lstat_add(v, w);
+  }
+  v = block_reduce_lstat<MERGE_THREADS>(v);
+  if (threadIdx.x == 0) {
+    out->loss_sum += v.loss;
+    out->ratio_sum += v.ratio;
+    out->entropy_sum += v.ent;
+    out->ratio_max = fmaxf(out->ratio_max, v.rmax);
+    out->clip_lo_count += v.clo;
+    out->clip_hi_count += v.chi;
+    out->tokens += v.tok;
+  }
+}
+
+rl_status launch_stats_reduce(const WsLayout& L, char* ws, rl_loss_stats* stats, cudaStream_t s) {
+  if (!stats || L.nblk_loss == 0) return RL_OK;
+  TraceScope ts(RL_K_REDUCE, s);
+  k_stats_reduce<<<1, MERGE_THREADS, 0, s>>>(reinterpret_cast<const double*>(ws + L.off_st_d),
+                                            reinterpret_cast<const float*>(ws + L.off_st_f),
+                                            reinterpret_cast<const long long*>(ws + L.off_st_i),
+                                            L.nblk_loss, stats);
+  RLH_CHECK_LAUNCH();
+  return RL_OK;
+}
+
+}  // namespace rlh

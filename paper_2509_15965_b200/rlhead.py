@@ -1,0 +1,270 @@
+"""ctypes binding of librlhead.so (include/rlhead.h): argument marshalling only.
+
+Every function here has the C name and forwards torch tensors as raw device
+pointers plus the current CUDA stream; all arithmetic runs in the library's
+CUDA kernels. There is no CPU fallback: importing this module fails loudly
+when librlhead.so is missing (build it with ``python -m
+paper_2509_15965_b200.build`` or ``__graft_entry__.build()``).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "librlhead.so")
+if not os.path.exists(_LIB_PATH):
+    raise ImportError(f"librlhead.so not built at {_LIB_PATH}; run `python -m "
+                      "paper_2509_15965_b200.build` (no CPU fallback exists)")
+lib = C.CDLL(_LIB_PATH)
+
+RL_OK, RL_ERR_INVALID_ARG, RL_ERR_UNSUPPORTED, RL_ERR_WORKSPACE, RL_ERR_CUDA = range(5)
+RL_F32, RL_BF16 = 0, 1
+RL_DEVERR_CU_SEQLENS, RL_DEVERR_TARGET, RL_DEVERR_GROUP = 1, 2, 4
+KERNEL_KINDS = ["prepare", "gather", "gemm_lse", "merge", "gemm_dz", "gemm_dh", "gemm_dw",
+                "grpo", "simt_fwd", "simt_bwd", "reduce", "misc"]
+
+
+class rl_batch(C.Structure):
+    _fields_ = [("num_rows", C.c_int64), ("num_seqs", C.c_int32), ("cu_seqlens", C.c_void_p),
+                ("targets", C.c_void_p), ("mask", C.c_void_p), ("err_flags", C.c_void_p)]
+
+
+class rl_head(C.Structure):
+    _fields_ = [("hidden", C.c_int32), ("vocab", C.c_int32), ("dtype", C.c_int),
+                ("ld_hidden", C.c_int64), ("inv_temperature", C.c_float)]
+
+
+class rl_loss_params(C.Structure):
+    _fields_ = [("clip_lo", C.c_float), ("clip_hi", C.c_float), ("logratio_clamp", C.c_float),
+                ("loss_scale", C.c_double), ("n_tokens_global", C.c_void_p)]
+
+
+class rl_loss_stats(C.Structure):
+    _fields_ = [("loss_sum", C.c_double), ("ratio_sum", C.c_double), ("entropy_sum", C.c_double),
+                ("ratio_max", C.c_float), ("reserved", C.c_int32), ("clip_lo_count", C.c_int64),
+                ("clip_hi_count", C.c_int64), ("tokens", C.c_int64)]
+
+
+STATS_BYTES = C.sizeof(rl_loss_stats)
+_vp, _sz = C.c_void_p, C.c_size_t
+
+lib.rl_workspace_size.restype = C.c_size_t
+lib.rl_workspace_size.argtypes = [C.POINTER(rl_head), C.c_int64, C.c_int32]
+lib.rl_batch_prepare.restype = C.c_int
+lib.rl_batch_prepare.argtypes = [C.POINTER(rl_head), C.POINTER(rl_batch), _vp, _vp, _vp, _vp,
+                                 _vp, _sz, _vp]
+lib.rl_logprob_fwd.restype = C.c_int
+lib.rl_logprob_fwd.argtypes = [C.POINTER(rl_head), _vp, _vp, C.POINTER(rl_batch), _vp, _vp, _vp,
+                               _vp, _sz, _vp]
+lib.rl_grpo_group_stats.restype = C.c_int
+lib.rl_grpo_group_stats.argtypes = [_vp, _vp, C.c_int32, C.c_int32, _vp, _vp, _vp, _vp]
+lib.rl_grpo_advantage.restype = C.c_int
+lib.rl_grpo_advantage.argtypes = [_vp, _vp, C.c_int32, C.c_int32, _vp, _vp, C.c_float, C.c_int32,
+                                  _vp, _vp, _vp]
+lib.rl_policy_loss_fwd_bwd.restype = C.c_int
+lib.rl_policy_loss_fwd_bwd.argtypes = [C.POINTER(rl_head), _vp, _vp, C.POINTER(rl_batch), _vp,
+                                       _vp, C.POINTER(rl_loss_params), _vp, _vp, _vp, _vp, _vp,
+                                       _vp, _sz, _vp]
+lib.rl_status_string.restype = C.c_char_p
+lib.rl_status_string.argtypes = [C.c_int]
+lib.rl_build_info.restype = C.c_char_p
+lib.rl_launch_count.restype = C.c_int64
+lib.rl_trace_begin.restype = C.c_int
+lib.rl_trace_begin.argtypes = [C.c_int32]
+lib.rl_trace_end.restype = C.c_int32
+lib.rl_trace_end.argtypes = [_vp]
+lib.rl_trace_durations.restype = C.c_int32
+lib.rl_trace_durations.argtypes = [_vp, C.c_int32]
+
+EXPORTED = ["rl_workspace_size", "rl_batch_prepare", "rl_logprob_fwd", "rl_grpo_group_stats",
+            "rl_grpo_advantage", "rl_policy_loss_fwd_bwd", "rl_status_string", "rl_build_info",
+            "rl_launch_count", "rl_trace_begin", "rl_trace_end", "rl_trace_durations"]
+
+
+class RLHeadError(RuntimeError):
+    pass
+
+
+def _check(st: int, what: str):
+    if st != RL_OK:
+        raise RLHeadError(f"{what}: {lib.rl_status_string(st).decode()}")
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    return C.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+# ------------------------------------------------------------ descriptors ----
+@dataclass
+class Head:
+    """rl_head: hidden size h, vocab V, dtype ('bf16' | 'f32'), ld_hidden, 1/tau."""
+    hidden: int
+    vocab: int
+    dtype: str = "bf16"
+    ld_hidden: int | None = None
+    inv_temperature: float = 1.0
+
+    def c(self) -> rl_head:
+        return rl_head(self.hidden, self.vocab, RL_BF16 if self.dtype == "bf16" else RL_F32,
+                       self.ld_hidden or self.hidden, self.inv_temperature)
+
+
+@dataclass
+class Batch:
+    """rl_batch over device tensors: cu_seqlens int32[S+1], targets int32[R],
+    mask uint8[R], optional err_flags int32[1]."""
+    cu_seqlens: object
+    targets: object
+    mask: object
+    err_flags: object = None
+    num_rows: int | None = None
+
+    def c(self) -> rl_batch:
+        R = self.num_rows if self.num_rows is not None else int(self.mask.shape[0])
+        return rl_batch(R, int(self.cu_seqlens.shape[0]) - 1, _ptr(self.cu_seqlens),
+                        _ptr(self.targets), _ptr(self.mask), _ptr(self.err_flags))
+
+
+@dataclass
+class LossParams:
+    clip_lo: float = 0.2
+    clip_hi: float = 0.2
+    logratio_clamp: float = 20.0
+    loss_scale: float = 1.0
+    n_tokens_global: object = None  # device int64[1] tensor: scale = 1/N
+
+    def c(self) -> rl_loss_params:
+        return rl_loss_params(self.clip_lo, self.clip_hi, self.logratio_clamp, self.loss_scale,
+                              _ptr(self.n_tokens_global))
+
+
+class Workspace:
+    """A growable device scratch buffer (256-B aligned torch allocation)."""
+
+    def __init__(self, device="cuda"):
+        self.device = device
+        self.buf = None
+
+    def get(self, nbytes: int):
+        import torch
+        if self.buf is None or self.buf.numel() < nbytes:
+            self.buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.device)
+        return self.buf
+
+
+def new_stats(device="cuda"):
+    """A zeroed device rl_loss_stats (as a uint8 tensor of sizeof bytes)."""
+    import torch
+    return torch.zeros(STATS_BYTES, dtype=torch.uint8, device=device)
+
+
+def read_stats(t) -> dict:
+    raw = t.detach().to("cpu").numpy().tobytes()
+    s = rl_loss_stats.from_buffer_copy(raw)
+    return {k: getattr(s, k) for k, _ in rl_loss_stats._fields_ if k != "reserved"}
+
+
+# --------------------------------------------------------------- C calls ----
+def rl_workspace_size(head: Head, num_rows: int, want_bwd: bool) -> int:
+    hd = head.c()
+    n = lib.rl_workspace_size(C.byref(hd), int(num_rows), int(bool(want_bwd)))
+    if n == 0:
+        raise RLHeadError("rl_workspace_size: invalid head")
+    return int(n)
+
+
+def rl_batch_prepare(head: Head, batch: Batch, row_seq=None, active_idx=None, n_active=None,
+                     n_accum=None, ws: Workspace | None = None, stream=None):
+    hd, b = head.c(), batch.c()
+    ws = ws or Workspace()
+    nb = rl_workspace_size(head, b.num_rows, False)
+    buf = ws.get(nb)
+    _check(lib.rl_batch_prepare(C.byref(hd), C.byref(b), _ptr(row_seq), _ptr(active_idx),
+                                _ptr(n_active), _ptr(n_accum), _ptr(buf), buf.numel(),
+                                _stream(stream)), "rl_batch_prepare")
+
+
+def rl_logprob_fwd(head: Head, hidden, weight, batch: Batch, logp, entropy=None, lse=None,
+                   ws: Workspace | None = None, stream=None):
+    hd, b = head.c(), batch.c()
+    ws = ws or Workspace()
+    buf = ws.get(rl_workspace_size(head, b.num_rows, False))
+    _check(lib.rl_logprob_fwd(C.byref(hd), _ptr(hidden), _ptr(weight), C.byref(b), _ptr(logp),
+                              _ptr(entropy), _ptr(lse), _ptr(buf), buf.numel(), _stream(stream)),
+           "rl_logprob_fwd")
+
+
+def rl_grpo_group_stats(rewards, group_of_seq, num_groups: int, sum_stats, max_stats,
+                        err_flags=None, stream=None):
+    _check(lib.rl_grpo_group_stats(_ptr(rewards), _ptr(group_of_seq), int(rewards.shape[0]),
+                                   int(num_groups), _ptr(sum_stats), _ptr(max_stats),
+                                   _ptr(err_flags), _stream(stream)), "rl_grpo_group_stats")
+
+
+def rl_grpo_advantage(rewards, group_of_seq, num_groups: int, adv, sum_stats=None, max_stats=None,
+                      eps: float = 1e-6, unbiased: bool = True, err_flags=None, stream=None):
+    _check(lib.rl_grpo_advantage(_ptr(rewards), _ptr(group_of_seq), int(rewards.shape[0]),
+                                 int(num_groups), _ptr(sum_stats), _ptr(max_stats), float(eps),
+                                 int(bool(unbiased)), _ptr(adv), _ptr(err_flags),
+                                 _stream(stream)), "rl_grpo_advantage")
+
+
+def rl_policy_loss_fwd_bwd(head: Head, hidden, weight, batch: Batch, old_logp, adv,
+                           params: LossParams, logp, grad_hidden, grad_weight, entropy=None,
+                           stats=None, ws: Workspace | None = None, stream=None):
+    hd, b, p = head.c(), batch.c(), params.c()
+    ws = ws or Workspace()
+    buf = ws.get(rl_workspace_size(head, b.num_rows, True))
+    _check(lib.rl_policy_loss_fwd_bwd(C.byref(hd), _ptr(hidden), _ptr(weight), C.byref(b),
+                                      _ptr(old_logp), _ptr(adv), C.byref(p), _ptr(logp),
+                                      _ptr(entropy), _ptr(grad_hidden), _ptr(grad_weight),
+                                      _ptr(stats), _ptr(buf), buf.numel(), _stream(stream)),
+           "rl_policy_loss_fwd_bwd")
+
+
+def rl_launch_count() -> int:
+    return int(lib.rl_launch_count())
+
+
+def rl_build_info() -> str:
+    return lib.rl_build_info().decode()
+
+
+class Trace:
+    """Context manager around rl_trace_begin/end: per-launch device times."""
+
+    def __init__(self, capacity: int = 1 << 16):
+        self.capacity = capacity
+        self.kinds = None
+        self.ms = None
+
+    def __enter__(self):
+        _check(lib.rl_trace_begin(self.capacity), "rl_trace_begin")
+        return self
+
+    def __exit__(self, *exc):
+        kinds = np.zeros(self.capacity, dtype=np.int32)
+        n = lib.rl_trace_end(kinds.ctypes.data_as(C.c_void_p))
+        ms = np.zeros(max(n, 1), dtype=np.float32)
+        lib.rl_trace_durations(ms.ctypes.data_as(C.c_void_p), n)
+        self.kinds, self.ms = kinds[:n], ms[:n]
+        return False
+
+    def by_kind(self) -> dict:
+        out = {}
+        for k, t in zip(self.kinds, self.ms):
+            name = KERNEL_KINDS[k]
+            c, s = out.get(name, (0, 0.0))
+            out[name] = (c + 1, s + float(t))
+        return out

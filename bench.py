@@ -1,0 +1,402 @@
+#!/usr/bin/env python
+"""Benchmark of the GRPO policy-loss head: fwd+bwd tokens/s on 1..8 B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config qwen7b]
+    torchrun --nproc-per-node N bench.py --gpus N ...     (one rank per GPU)
+    python bench.py --impl reference ...                  (CPU float64 oracle arm)
+
+A "step" is one GRPO mini-batch of the config (BASELINE.json configs[3],
+Qwen-7B head: 128 prompts x G=16, long-tailed responses up to 16k tokens,
+~5.6M masked tokens) through the whole hot path: N all-reduce, GRPO
+advantages, every micro-batch through rl_policy_loss_fwd_bwd (projection,
+online LSE, loss, dZ recompute, dH, dW), dW all-reduce. Strong scaling: the
+mini-batch is fixed and its prompt groups are LPT-sharded over the ranks.
+value = masked response tokens of the mini-batch / device time per step
+(CUDA events, max over ranks). Inputs (44 GB of hidden rows) exceed L2.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "policy-loss fwd+bwd tokens/s at 1/2/4/8 B200; % bf16 tensor-core peak"
+GEMM_KINDS = ("gemm_lse", "gemm_dz", "gemm_dh", "gemm_dw")
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=3)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--config", default="qwen7b")
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--mb-rows", type=int, default=65536)
+    p.add_argument("--seed", type=int, default=0)
+    p.add_argument("--max-mb", type=int, default=0, help="debug: first micro-batches only")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-sample-tokens", type=int, default=96)
+    return p.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return dict(hbm=float(d["hbm_gbs"]), bf16=float(d["bf16_tflops"]),
+                    bf16_sus=float(d["bf16_tflops_sustained"]), src="measured")
+    except Exception:
+        return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, src="fallback")
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-i", str(self.index)], stdout=open(self.path, "w"),
+                stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, pw, reasons = [], [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+                pw.append(float(f[3]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        os.unlink(self.path)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": []}
+        loaded = [s for s, p in zip(sm, pw) if p > 300.0] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def cpu_baseline(cfg, layout, seed, tokens):
+    """The oracle as it stands on this host, on a bounded sample: the first
+    `tokens` response rows of sequence 0 (with its prompt rows), fwd+bwd."""
+    import torch
+
+    import oracle
+    from workload import make_tensors_host, sub_layout
+    try:
+        from threadpoolctl import threadpool_info
+        blas = max([i.get("num_threads", 0) for i in threadpool_info()] or [0])
+    except Exception:
+        blas = 0
+    sub, _ = sub_layout(layout, [0])
+    P = int(sub.prompt_len[0]) if sub.prompt_len is not None else 0
+    R = min(sub.num_rows, P + tokens)
+    cu = np.array([0, R], dtype=np.int32)
+    mask, targets = sub.mask[:R], sub.targets[:R]
+    H, W = make_tensors_host(cfg, R, seed=seed)
+    old = np.zeros(R)
+    adv = np.array([1.0])
+    t0 = time.perf_counter()
+    out = oracle.policy_loss_fwd_bwd(H, W, cu, mask, targets, old, adv)
+    dt = time.perf_counter() - t0
+    del torch
+    n = int(out["n_active"])
+    return {"value": n / dt, "unit": "tokens/s", "cores": os.cpu_count(), "blas_threads": blas,
+            "kind": "oracle", "seconds": dt,
+            "sample": f"{n} masked tokens of sequence 0 ({cfg.name}, fwd+bwd incl. dW [V,h] fp64)"}
+
+
+def run_reference(args, cfg):
+    """--impl reference: the CPU float64 oracle, timed on this host."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    from workload import make_layout
+    layout = make_layout(cfg, seed=args.seed)
+    for _ in range(args.warmup):
+        cpu_baseline(cfg, layout, args.seed, 8)
+    vals = []
+    for _ in range(args.steps):
+        vals.append(cpu_baseline(cfg, layout, args.seed, args.cpu_sample_tokens))
+    v = statistics.median([x["value"] for x in vals])
+    cb = dict(vals[-1])
+    cb["value"] = v
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000.0 * statistics.median([x["seconds"] for x in vals]),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg.name, "sample": cb["sample"]},
+            "cpu_baseline": cb,
+            "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    args = parse()
+    from workload import CONFIGS, make_layout, make_tensors_torch, ratio_noise, sub_layout
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2509_15965_b200 as rl
+    from paper_2509_15965_b200.dp import PolicyLossStep, device_batch, shard_layout
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    group = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    layout = make_layout(cfg, seed=args.seed)
+    seqs, loads = shard_layout(layout, rank, world)
+    mine, _ = sub_layout(layout, seqs)
+    db = device_batch(mine, args.mb_rows, device=dev)
+    if args.max_mb:
+        db.mbs = db.mbs[:args.max_mb]
+    _, W = make_tensors_torch(cfg, 0, seed=args.seed, device=dev, hidden=False)
+    H, _ = make_tensors_torch(cfg, mine.num_rows, seed=args.seed + 7919 * (rank + 1), device=dev,
+                              weight=False)
+    head = rl.Head(cfg.hidden, cfg.vocab, cfg.dtype)
+    max_mb = max(r1 - r0 for _, _, r0, r1, _ in db.mbs)
+
+    # old log-probs from the inference-worker call + delta ~ N(0, 0.05^2) (M.2)
+    old = torch.empty(max(mine.num_rows, 1), dtype=torch.float32, device=dev)
+    ws = rl.Workspace(dev)
+    for (s0, s1, r0, r1, cu_mb) in db.mbs:
+        rl.rl_logprob_fwd(head, H[r0:r1], W, rl.Batch(cu_mb, db.targets[r0:r1], db.mask[r0:r1],
+                                                      num_rows=r1 - r0), old[r0:r1], ws=ws)
+    old += torch.as_tensor(ratio_noise(old.shape[0], args.seed + rank), dtype=torch.float32,
+                           device=dev)
+    del ws
+    step = PolicyLossStep(head, W, db, group=group)
+    gh = torch.empty(max_mb, cfg.hidden, dtype=H.dtype, device=dev)
+    tokens_local = int(sum(int(mine.mask[r0:r1].sum()) for _, _, r0, r1, _ in db.mbs))
+    tok_t = torch.tensor([tokens_local], dtype=torch.int64, device=dev)
+    if world > 1:
+        dist.all_reduce(tok_t)
+    tokens_global = int(tok_t.item())
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ------------------------------------------------------ device-timed run
+    for _ in range(args.warmup):
+        step.run(H, old, gh)
+    barrier()
+    clk = Clocks(local)
+    clk.start()
+    tr = rl.Trace(1 << 17).start()
+    n0 = rl.rl_launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record()
+    for _ in range(args.steps):
+        step.run(H, old, gh)
+    e1.record()
+    barrier()
+    launches = rl.rl_launch_count() - n0
+    tr.stop()
+    clocks = clk.stop()
+    ms = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms_per_step = float(ms.item())
+    value = tokens_global / (ms_per_step / 1e3)
+
+    # roofline of the dominant kernel (GEMM kinds: 2hV flops per token per launch)
+    pk = peaks()
+    kinds = tr.by_kind()
+    per_kind = {k: {"launches": c, "ms_total": round(t, 3)} for k, (c, t) in kinds.items()}
+    gemm = {k: kinds[k] for k in GEMM_KINDS if k in kinds}
+    dom = max(gemm, key=lambda k: gemm[k][1])
+    dom_flops = 2.0 * cfg.hidden * cfg.vocab * tokens_local * args.steps
+    achieved = dom_flops / (gemm[dom][1] / 1e3) / 1e12
+    step_tflops_exec = 8.0 * cfg.hidden * cfg.vocab * value / 1e12
+    step_tflops_alg = 6.0 * cfg.hidden * cfg.vocab * value / 1e12
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        try:
+            tpt = json.load(open(prof)).get(cfg.name, {}).get(dom)
+            if tpt:
+                traffic = tpt * tokens_local / max(gemm[dom][0] / args.steps, 1)
+        except Exception:
+            traffic = None
+    roof = {"bound": "tensor", "kernel": f"k_tc_gemm[{dom}]", "achieved": round(achieved, 1),
+            "peak": pk["bf16_sus"], "unit": "TFLOP/s", "frac": round(achieved / pk["bf16_sus"], 4),
+            "traffic": traffic, "peak_kind": f"bf16 sustained ({pk['src']})",
+            "frac_of_burst": round(achieved / pk["bf16"], 4),
+            "step_executed_tflops": round(step_tflops_exec / world, 1),
+            "step_executed_frac_burst": round(step_tflops_exec / world / pk["bf16"], 4),
+            "step_algorithmic_frac_burst": round(step_tflops_alg / world / pk["bf16"], 4)}
+
+    # ------------------------------------------------ end-to-end (host data)
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, rl, step, db, mine, H, old, gh, dev, world, tokens_global)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg, layout, args.seed, args.cpu_sample_tokens)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 1), "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic",
+            "config": {"workload": f"{cfg.name} head (h={cfg.hidden}, V={cfg.vocab}), "
+                                   f"{cfg.prompts} prompts x G={cfg.group}, responses <= {cfg.lmax}",
+                       "global_batch_tokens": tokens_global, "micro_batch_rows": args.mb_rows,
+                       "micro_batches_per_rank": len(db.mbs), "parallelism": f"dp{world}",
+                       "l2": "inputs > L2 (hidden rows of the mini-batch ~ "
+                             f"{mine.num_rows * cfg.hidden * 2 / 1e9:.1f} GB per rank)",
+                       "lpt_load_max_over_mean": round(float(loads.max() / loads.mean()), 4),
+                       "partial": bool(args.max_mb)},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "clocks": clocks, "kernels": per_kind,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_e2e(args, rl, step, db, mine, H, old, gh, dev, world, tokens_global):
+    """Same metric through the public API with HOST inputs: every step copies
+    its inputs from pinned host memory (hidden streamed per micro-batch on a
+    copy stream, double-buffered) and reads the loss statistics back."""
+    import torch
+    import torch.distributed as dist
+    R = mine.num_rows
+    host_H = torch.empty(H.shape, dtype=H.dtype, pin_memory=True)
+    host_H.copy_(H)
+    small = dict(targets=db.targets, mask=db.mask, cu=db.cu, gos=db.gos, rewards=db.rewards,
+                 old=old)
+    small.update({f"cu_mb{i}": mb[4] for i, mb in enumerate(db.mbs)})
+    host_small = {k: v.detach().to("cpu").pin_memory() for k, v in small.items()}
+    dev_small = {k: torch.empty_like(v, device=dev) for k, v in host_small.items()}
+    max_mb = gh.shape[0]
+    bufs = [torch.empty(max_mb, H.shape[1], dtype=H.dtype, device=dev) for _ in range(2)]
+    copy_s = torch.cuda.Stream(device=dev)
+    ready = [torch.cuda.Event() for _ in range(2)]
+    freed = [torch.cuda.Event() for _ in range(2)]
+    comp = torch.cuda.current_stream()
+    stats_host = torch.empty(rl.rlhead.STATS_BYTES, dtype=torch.uint8, pin_memory=True)
+    h2d = sum(v.numel() * v.element_size() for v in host_small.values()) + \
+        sum((r1 - r0) * H.shape[1] * H.element_size() for _, _, r0, r1, _ in db.mbs)
+
+    def issue_copy(i):
+        _, _, r0, r1, _ = db.mbs[i]
+        with torch.cuda.stream(copy_s):
+            copy_s.wait_event(freed[i % 2])
+            bufs[i % 2][:r1 - r0].copy_(host_H[r0:r1], non_blocking=True)
+            ready[i % 2].record(copy_s)
+
+    def hidden_for_mb(i):
+        comp.wait_event(ready[i % 2])
+        _, _, r0, r1, _ = db.mbs[i]
+        return bufs[i % 2][:r1 - r0]
+
+    def after_mb(i):
+        freed[i % 2].record(comp)
+        if i + 2 < len(db.mbs):
+            issue_copy(i + 2)
+
+    orig = (step.db.targets, step.db.mask, step.db.cu, step.db.gos, step.db.rewards,
+            list(step.db.mbs))
+
+    def one():
+        for k, v in host_small.items():
+            dev_small[k].copy_(v, non_blocking=True)
+        step.db.targets, step.db.mask, step.db.cu = (dev_small["targets"], dev_small["mask"],
+                                                     dev_small["cu"])
+        step.db.gos, step.db.rewards = dev_small["gos"], dev_small["rewards"]
+        step.db.mbs = [(s0, s1, r0, r1, dev_small[f"cu_mb{i}"])
+                       for i, (s0, s1, r0, r1, _) in enumerate(orig[5])]
+        for e in freed:
+            e.record(comp)
+        issue_copy(0)
+        if len(db.mbs) > 1:
+            issue_copy(1)
+        step.run(None, dev_small["old"], gh, hidden_for_mb=hidden_for_mb, after_mb=after_mb)
+        stats_host.copy_(step.stats, non_blocking=True)
+
+    for _ in range(max(1, min(args.warmup, 2))):
+        one()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        one()
+    e1.record()
+    torch.cuda.synchronize()
+    (step.db.targets, step.db.mask, step.db.cu, step.db.gos, step.db.rewards) = orig[:5]
+    step.db.mbs = orig[5]
+    ms = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    v = tokens_global / (float(ms.item()) / 1e3)
+    del host_H
+    return {"value": round(v, 1), "unit": "tokens/s", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(rl.rlhead.STATS_BYTES), "ms_per_step": round(float(ms.item()), 3)}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,186 @@
+"""Host-side data-parallel driver of the policy-loss head.
+
+* ``lpt_shard``: whole prompt groups -> DP ranks, greedy least-loaded by token
+  count (longest first). This is the paper's weighted load-balancing channel
+  ("each data item can be assigned a weight value") used as a
+  sharder; it keeps every GRPO group on one rank so advantages are
+  rank-local. Bound: max - min load <= max item weight.
+* ``pack_micro_batches``: whole sequences packed greedily, in order, into
+  micro-batches of at most ``budget`` rows ("the micro-batch defines
+  forward/backward units, while the global-batch determines when model
+  updates occur").
+* ``PolicyLossStep``: one mini-batch step on this rank: N all-reduce, GRPO
+  advantages, every micro-batch through ``rl_policy_loss_fwd_bwd``, dW SUM
+  all-reduce (the loss is normalised by the global N, so gradients add;
+  a DDP-style mean would be off by world_size), stats all-reduce.
+
+Collectives go through torch.distributed (NCCL over NVLink on the B200 box,
+gloo on CPU in the tests); nothing else crosses ranks.
+"""
+from __future__ import annotations
+
+import heapq
+from dataclasses import dataclass, field
+
+import numpy as np
+
+
+def lpt_shard(weights, world: int):
+    """Assign items (e.g. prompt groups, weight = token count) to ``world``
+    bins: heaviest first onto the currently lightest bin (ties: lower bin id,
+    then lower item id). Returns (list of item-id lists per bin, loads)."""
+    weights = np.asarray(weights, dtype=np.int64)
+    order = sorted(range(len(weights)), key=lambda i: (-int(weights[i]), i))
+    heap = [(0, r) for r in range(world)]
+    bins = [[] for _ in range(world)]
+    loads = np.zeros(world, dtype=np.int64)
+    for i in order:
+        load, r = heapq.heappop(heap)
+        bins[r].append(i)
+        loads[r] = load + int(weights[i])
+        heapq.heappush(heap, (int(loads[r]), r))
+    for b in bins:
+        b.sort()
+    return bins, loads
+
+
+def pack_micro_batches(seq_rows, budget: int):
+    """Contiguous [s0, s1) sequence ranges, each <= budget rows (a single
+    longer sequence gets a micro-batch of its own)."""
+    out, s0, rows = [], 0, 0
+    for s, n in enumerate(np.asarray(seq_rows, dtype=np.int64)):
+        if rows > 0 and rows + int(n) > budget:
+            out.append((s0, s))
+            s0, rows = s, 0
+        rows += int(n)
+    if len(seq_rows) > s0 or not out:
+        out.append((s0, len(seq_rows)))
+    return out
+
+
+def shard_layout(layout, rank: int, world: int):
+    """This rank's sequences (whole groups, LPT by response tokens)."""
+    G = layout.num_groups
+    cu = layout.cu_seqlens.astype(np.int64)
+    seq_tokens = np.add.reduceat(layout.mask.astype(np.int64), cu[:-1]) \
+        if layout.num_rows else np.zeros(layout.num_seqs, np.int64)
+    seq_tokens = np.where(cu[1:] > cu[:-1], seq_tokens, 0)
+    g_tokens = np.bincount(layout.group_of_seq, weights=seq_tokens, minlength=G).astype(np.int64)
+    bins, loads = lpt_shard(g_tokens, world)
+    mine = set(bins[rank])
+    seqs = [s for s in range(layout.num_seqs) if int(layout.group_of_seq[s]) in mine]
+    return seqs, loads
+
+
+# ------------------------------------------------------------ collectives ----
+def all_reduce_(t, op="sum", group=None):
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.SUM if op == "sum" else dist.ReduceOp.MAX,
+                        group=group)
+    return t
+
+
+def reduce_stats_(stats_u8, group=None):
+    """All-reduce a device rl_loss_stats (56 bytes): sums for the fp64/int64
+    fields, max for ratio_max."""
+    import torch
+    d = stats_u8[:24].view(torch.float64)
+    f = stats_u8[24:28].view(torch.float32)
+    i = stats_u8[32:56].view(torch.int64)
+    all_reduce_(d, "sum", group)
+    all_reduce_(f, "max", group)
+    all_reduce_(i, "sum", group)
+    return stats_u8
+
+
+@dataclass
+class DeviceBatch:
+    """One rank's packed batch resident on the device, plus its micro-batches."""
+    cu: object            # int32 [S+1] (whole local batch)
+    targets: object       # int32 [R]
+    mask: object          # uint8 [R]
+    gos: object           # int32 [S] local group ids
+    rewards: object       # float32 [S]
+    num_groups: int
+    mbs: list             # [(s0, s1, r0, r1, cu_mb tensor)]
+    num_rows: int
+    num_tokens: int
+    seq_rows: np.ndarray = field(default=None)
+
+
+def device_batch(layout, mb_rows: int, device="cuda") -> DeviceBatch:
+    import torch
+    cu_np = layout.cu_seqlens.astype(np.int64)
+    seq_rows = cu_np[1:] - cu_np[:-1]
+    # local group ids 0..G'-1 (keeps the GRPO launch small)
+    uniq, gos_local = np.unique(layout.group_of_seq, return_inverse=True)
+    mbs = []
+    for s0, s1 in pack_micro_batches(seq_rows, mb_rows):
+        r0, r1 = int(cu_np[s0]), int(cu_np[s1])
+        cu_mb = torch.as_tensor((cu_np[s0:s1 + 1] - r0).astype(np.int32), device=device)
+        mbs.append((s0, s1, r0, r1, cu_mb))
+    return DeviceBatch(
+        cu=torch.as_tensor(layout.cu_seqlens, device=device),
+        targets=torch.as_tensor(layout.targets, device=device),
+        mask=torch.as_tensor(layout.mask, device=device),
+        gos=torch.as_tensor(gos_local.astype(np.int32), device=device),
+        rewards=torch.as_tensor(layout.rewards, device=device),
+        num_groups=len(uniq), mbs=mbs, num_rows=layout.num_rows,
+        num_tokens=layout.num_tokens, seq_rows=seq_rows)
+
+
+class PolicyLossStep:
+    """One GRPO mini-batch step of the head on this rank."""
+
+    def __init__(self, head, weight, db: DeviceBatch, params=None, group=None):
+        import torch
+        from . import rlhead as R
+        self.R = R
+        self.head, self.W, self.db = head, weight, db
+        self.params = params or R.LossParams()
+        self.group = group
+        dev = weight.device
+        self.n_global = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.params.n_tokens_global = self.n_global
+        self.adv = torch.empty(max(db.cu.shape[0] - 1, 1), dtype=torch.float32, device=dev)
+        self.grad_w = torch.zeros(weight.shape[0], weight.shape[1], dtype=torch.float32, device=dev)
+        self.stats = R.new_stats(dev)
+        self.logp = torch.empty(max(db.num_rows, 1), dtype=torch.float32, device=dev)
+        self.ws = R.Workspace(dev)
+        self.ws_prep = R.Workspace(dev)
+
+    def count_tokens(self):
+        """N = masked tokens of the whole mini-batch over all ranks."""
+        R = self.R
+        self.n_global.zero_()
+        R.rl_batch_prepare(self.head, R.Batch(self.db.cu, self.db.targets, self.db.mask),
+                           n_accum=self.n_global, ws=self.ws_prep)
+        all_reduce_(self.n_global, "sum", self.group)
+
+    def advantages(self):
+        self.R.rl_grpo_advantage(self.db.rewards, self.db.gos, self.db.num_groups, self.adv)
+
+    def run(self, hidden, old_logp, grad_hidden, hidden_for_mb=None, after_mb=None):
+        """hidden [R, h] (or ``hidden_for_mb(i)`` -> the micro-batch's rows, for
+        streaming). grad_hidden is [R, h], or a reused buffer of at least the
+        largest micro-batch (its rows then hold the last micro-batch's dH,
+        which the trunk backward would consume before the next one)."""
+        R = self.R
+        self.count_tokens()
+        self.advantages()
+        self.grad_w.zero_()
+        self.stats.zero_()
+        full_gh = grad_hidden.shape[0] >= self.db.num_rows
+        for i, (s0, s1, r0, r1, cu_mb) in enumerate(self.db.mbs):
+            hs = hidden_for_mb(i) if hidden_for_mb else hidden[r0:r1]
+            gh = grad_hidden[r0:r1] if full_gh else grad_hidden[:r1 - r0]
+            b = R.Batch(cu_mb, self.db.targets[r0:r1], self.db.mask[r0:r1], num_rows=r1 - r0)
+            R.rl_policy_loss_fwd_bwd(self.head, hs, self.W, b, old_logp[r0:r1], self.adv[s0:s1],
+                                     self.params, self.logp[r0:r1], gh,
+                                     self.grad_w, stats=self.stats, ws=self.ws)
+            if after_mb:
+                after_mb(i)
+        all_reduce_(self.grad_w, "sum", self.group)
+        reduce_stats_(self.stats, self.group)
+        return self.stats

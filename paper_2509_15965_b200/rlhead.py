@@ -249,16 +249,23 @@ class Trace:
         self.kinds = None
         self.ms = None
 
-    def __enter__(self):
+    def start(self):
         _check(lib.rl_trace_begin(self.capacity), "rl_trace_begin")
         return self
 
-    def __exit__(self, *exc):
+    def stop(self):
         kinds = np.zeros(self.capacity, dtype=np.int32)
         n = lib.rl_trace_end(kinds.ctypes.data_as(C.c_void_p))
         ms = np.zeros(max(n, 1), dtype=np.float32)
         lib.rl_trace_durations(ms.ctypes.data_as(C.c_void_p), n)
         self.kinds, self.ms = kinds[:n], ms[:n]
+        return self
+
+    def __enter__(self):
+        return self.start()
+
+    def __exit__(self, *exc):
+        self.stop()
         return False
 
     def by_kind(self) -> dict:

@@ -161,10 +161,16 @@ def test_tiny_fp32_loss_fwd_bwd(rl):
     ref = oracle.policy_loss_fwd_bwd(H, W, lay.cu_seqlens, lay.mask, lay.targets, old,
                                      adv.astype(np.float32), n_global=N)
     np.testing.assert_allclose(out["logp"], ref["logp"], atol=1e-5, rtol=0)
-    assert out["stats"]["loss_sum"] == pytest.approx(ref["loss_sum"], rel=1e-5, abs=1e-6)
+    # the 1e-5 logp budget propagates through r = e^{logp-old}:
+    # |dl_t| <= |A_t| r_t * 1e-5, so |dL_sum| <= 1e-5 * sum_t |A_t| r_t, and
+    # the gradients (linear in g_t = -A r / N) get a 2e-5 relative budget.
+    seq = np.searchsorted(lay.cu_seqlens, np.arange(lay.num_rows), side="right") - 1
+    act = lay.mask.astype(bool)
+    budget = 1e-5 * np.sum(np.abs(adv[seq][act]) * np.exp(ref["logp"][act] - old[act]))
+    assert abs(out["stats"]["loss_sum"] - ref["loss_sum"]) <= budget + 1e-7
     assert out["stats"]["tokens"] == N
-    assert rel_fro(out["dH"], ref["dH"]) <= 1e-5
-    assert rel_fro(out["dW"], ref["dW"]) <= 1e-5
+    assert rel_fro(out["dH"], ref["dH"]) <= 2e-5
+    assert rel_fro(out["dW"], ref["dW"]) <= 2e-5
     assert (out["dH"][lay.mask == 0] == 0).all()
 
 
@@ -240,10 +246,11 @@ def test_qwen15b_head_subbatch(rl):
     adv = np.array([1.25, -0.5], dtype=np.float32)
     ref_f = oracle.logprob_fwd(H, W, lay.cu_seqlens, lay.mask, lay.targets)
     old = guarded_old_logp(ref_f["logp"], np.random.default_rng(7))
-    out = _run_loss(rl, head, H.cuda(), W.cuda(), d, lay, old, adv)
+    out = _run_loss(rl, head, H.cuda(), W.cuda(), d, lay, old, adv, n_global=lay.num_tokens)
     ref = oracle.policy_loss_fwd_bwd(H, W, lay.cu_seqlens, lay.mask, lay.targets, old, adv)
     assert np.abs(out["logp"] - ref["logp"]).max() <= 2e-3
     assert np.abs(out["entropy"] - ref["entropy"]).max() <= 2e-3
+    assert out["stats"]["loss_sum"] == pytest.approx(ref["loss_sum"], rel=1e-2)
     assert rel_fro(out["dH"], ref["dH"]) <= 1e-2
     assert rel_fro(out["dW"], ref["dW"]) <= 1e-2 and max_rel(out["dW"], ref["dW"]) <= 1e-2
 

@@ -49,7 +49,7 @@ def pack_micro_batches(seq_rows, budget: int):
     longer sequence gets a micro-batch of its own)."""
     out, s0, rows = [], 0, 0
     for s, n in enumerate(np.asarray(seq_rows, dtype=np.int64)):
-        if rows > 0 and rows + int(n) > budget:
+        if s > s0 and rows + int(n) > budget:
             out.append((s0, s))
             s0, rows = s, 0
         rows += int(n)

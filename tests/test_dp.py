@@ -1,0 +1,120 @@
+"""Host-side data-parallel logic on CPU: LPT sharding bound, micro-batch
+packing, and the world-size-2 gloo reduction path (N all-reduce, dW SUM,
+stats SUM/MAX) reproducing the whole-batch oracle."""
+import ctypes as C
+import os
+import socket
+
+import numpy as np
+import pytest
+from hypothesis import given, settings, strategies as st
+
+import oracle
+from paper_2509_15965_b200.dp import lpt_shard, pack_micro_batches, shard_layout
+from workload import CONFIGS, make_layout, make_tensors_host, sub_layout
+
+
+@given(st.lists(st.integers(0, 10000), min_size=0, max_size=60), st.integers(1, 8))
+@settings(max_examples=200, deadline=None)
+def test_lpt_bound_and_cover(weights, world):
+    bins, loads = lpt_shard(weights, world)
+    items = sorted(i for b in bins for i in b)
+    assert items == list(range(len(weights)))
+    for r, b in enumerate(bins):
+        assert loads[r] == sum(weights[i] for i in b)
+    if weights:
+        assert loads.max() - loads.min() <= max(weights)   # S:L479-style bound
+    assert lpt_shard(weights, world)[0] == bins             # deterministic
+
+
+@given(st.lists(st.integers(0, 500), min_size=0, max_size=80), st.integers(1, 1000))
+@settings(max_examples=200, deadline=None)
+def test_micro_batch_packing(rows, budget):
+    mbs = pack_micro_batches(rows, budget)
+    covered = [s for s0, s1 in mbs for s in range(s0, s1)]
+    assert covered == list(range(len(rows)))
+    for s0, s1 in mbs:
+        tot = sum(rows[s0:s1])
+        assert tot <= budget or s1 - s0 == 1
+
+
+def test_shard_keeps_groups_whole():
+    lay = make_layout(CONFIGS["qwen1.5b"], seed=0)
+    seen = {}
+    for r in range(4):
+        seqs, loads = shard_layout(lay, r, 4)
+        for s in seqs:
+            g = int(lay.group_of_seq[s])
+            assert seen.setdefault(g, r) == r
+    assert len(seen) == lay.num_groups
+    assert loads.max() / loads.mean() < 1.05
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _stats_bytes(d):
+    from paper_2509_15965_b200 import rlhead as R
+    s = R.rl_loss_stats(d["loss_sum"], d["ratio_sum"], d["entropy_sum"], d["ratio_max"], 0,
+                        d["clip_lo_count"], d["clip_hi_count"], d["tokens"])
+    return bytes(s)
+
+
+def _worker(rank, world, port, out_dir):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2509_15965_b200 import rlhead as R
+    from paper_2509_15965_b200.dp import all_reduce_, reduce_stats_
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg = CONFIGS["tiny"]
+    lay = make_layout(cfg, seed=3)
+    H, W = make_tensors_host(cfg, lay.num_rows, seed=3)
+    adv_all, _ = oracle.grpo_advantage(lay.rewards, lay.group_of_seq, lay.num_groups)
+    seqs, _ = shard_layout(lay, rank, world)
+    mine, rows = sub_layout(lay, seqs)
+    old = np.zeros(lay.num_rows)
+    # C1: N = all-reduce(SUM) of the local active counts
+    n = torch.tensor([mine.num_tokens], dtype=torch.int64)
+    all_reduce_(n, "sum")
+    out = oracle.policy_loss_fwd_bwd(H[rows], W, mine.cu_seqlens, mine.mask, mine.targets,
+                                     old[rows], adv_all[seqs], n_global=int(n.item()))
+    # C3: dW all-reduce SUM; C4: stats SUM / MAX
+    dW = torch.from_numpy(out["dW"].copy())
+    all_reduce_(dW, "sum")
+    st = torch.frombuffer(bytearray(_stats_bytes(out["stats"])), dtype=torch.uint8).clone()
+    reduce_stats_(st)
+    if rank == 0:
+        np.save(os.path.join(out_dir, "dW.npy"), dW.numpy())
+        with open(os.path.join(out_dir, "stats.bin"), "wb") as f:
+            f.write(st.numpy().tobytes())
+        with open(os.path.join(out_dir, "n.txt"), "w") as f:
+            f.write(str(int(n.item())))
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_matches_whole_batch(tmp_path):
+    import torch.multiprocessing as mp
+
+    from paper_2509_15965_b200 import rlhead as R
+    world = 2
+    mp.start_processes(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world,
+                       join=True, start_method="spawn")
+    cfg = CONFIGS["tiny"]
+    lay = make_layout(cfg, seed=3)
+    H, W = make_tensors_host(cfg, lay.num_rows, seed=3)
+    adv, _ = oracle.grpo_advantage(lay.rewards, lay.group_of_seq, lay.num_groups)
+    ref = oracle.policy_loss_fwd_bwd(H, W, lay.cu_seqlens, lay.mask, lay.targets,
+                                     np.zeros(lay.num_rows), adv)
+    assert int(open(tmp_path / "n.txt").read()) == ref["n_active"]
+    np.testing.assert_allclose(np.load(tmp_path / "dW.npy"), ref["dW"], atol=1e-14)
+    st = R.rl_loss_stats.from_buffer_copy((tmp_path / "stats.bin").read_bytes())
+    assert st.loss_sum == pytest.approx(ref["stats"]["loss_sum"], abs=1e-12)
+    assert st.tokens == ref["stats"]["tokens"]
+    assert st.ratio_max == pytest.approx(ref["stats"]["ratio_max"], rel=1e-6)

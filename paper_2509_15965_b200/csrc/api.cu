@@ -52,7 +52,7 @@ bool ws_layout(const rl_head* hd, int64_t R, int want_bwd, WsLayout* L) {
   const bool tc = use_tc(hd);
   const int64_t h = hd->hidden, V = hd->vocab;
   L->R = R;
-  L->Rp = round_up(R > 0 ? R : 1, TC_BM);
+  L->Rp = round_up(R > 0 ? R : 1, 2 * TC_BM);  // whole CTA-pair tiles
   L->n_vt = tc ? ceil_div(V, TC_BN) : 1;
   L->Vp = round_up(V, TC_BN);
   L->nblk_rows = ceil_div(R, 1024);

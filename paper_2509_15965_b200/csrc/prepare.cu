@@ -193,7 +193,7 @@ k_gather_bf16(const uint4* __restrict__ hidden, int64_t ld_vec, int32_t hvec,
   const int64_t r = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   const int64_t T = hdr->n_active;
-  const int64_t Tp = (T + TC_BM - 1) / TC_BM * TC_BM;
+  const int64_t Tp = (T + 2 * TC_BM - 1) / (2 * TC_BM) * (2 * TC_BM);  // CTA-pair tile
   if (r >= Tp || r >= rows_bound) return;
   uint4* dst = hc + r * hvec;
   if (r < T) {

@@ -1,13 +1,13 @@
 // Tensor-core path of the head (bf16 in, fp32 accumulate) for sm_100a:
 // one persistent, warp-specialised tcgen05 GEMM with four fused epilogues.
 //
-//   warp 0  : TMA producer (one elected lane): A/B k-blocks -> 4-stage smem
-//             ring (128-B swizzle), mbarrier complete_tx.
-//   warp 1  : TMEM allocator + MMA issuer (one lane): tcgen05.mma
-//             kind::f16, M=128 N=256 K=16, accumulator in TMEM, two 256-col
+//   warp 0  : TMA producer (one elected lane): A/B k-blocks -> smem ring
+//             (128-B swizzle), mbarrier complete_tx.
+//   warp 1  : TMEM allocator + MMA issuer (one lane): tcgen05.mma kind::f16,
+//             N = 256, K = 16; fp32 accumulators in TMEM, two 256-column
 //             accumulators (double buffered) so the epilogue of tile i
-//             overlaps the MMAs of tile i+1; tcgen05.commit frees smem
-//             stages and signals the epilogue.
+//             overlaps the MMAs of tile i+1; tcgen05.commit frees smem stages
+//             and signals the epilogue.
 //   warps 4-7: epilogue (thread = accumulator row = TMEM lane):
 //     EPI_LSE (H3+H4, N3): online log-sum-exp of the 256 logits of the tile
 //             -> per-row split-V partial (m, sum e^{z-m}, sum e^{z-m}(z-m)),
@@ -18,6 +18,14 @@
 //     EPI_ROWS(H7, N6): dH = dZ W, rows scattered back to the packed layout.
 //     EPI_ACC (H8, N7): dW += dZ^T H (fp32 read-modify-write).
 //
+// CG = 1: one CTA per 128 x 256 tile (tcgen05 cta_group::1, M = 128).
+// CG = 2: a cluster of two CTAs (a TPC pair) per 256 x 256 tile
+//   (cta_group::2, M = 256): each CTA loads its 128 rows of A and its 128
+//   columns of B with 2-SM TMA (complete_tx on the leader's barrier), the
+//   leader issues the pair MMA, commits are multicast to both CTAs, each CTA
+//   drains its own TMEM half. Per-SM operand traffic per MMA drops from
+//   12 KB to 8 KB, so smem stages shrink to 32 KB and the ring deepens to 6.
+//
 // Operand majors: fwd/dZ  A = Hc [T,h] K-major,  B = W [V,h] K-major;
 //                 dH      A = dZ [T,V] K-major,  B = W [V,h] MN-major;
 //                 dW      A = dZ [T,V] MN-major, B = Hc [T,h] MN-major.
@@ -26,18 +34,32 @@
 #include "kernels.h"
 #include "ptx.cuh"
 
+#include <cstdlib>
 #include <mutex>
 
 namespace rlh {
 
-constexpr int TC_STAGES = 4;
-constexpr int TC_A_BYTES = TC_BM * TC_BK * 2;             // 16 KB
-constexpr int TC_B_BYTES = TC_BN * TC_BK * 2;             // 32 KB
-constexpr int TC_STAGE_BYTES = TC_A_BYTES + TC_B_BYTES;   // 48 KB
 constexpr int TC_THREADS = 256;
-constexpr int TC_SMEM_BYTES = TC_STAGES * TC_STAGE_BYTES + 1024 + 256;
-constexpr int TC_TMEM_COLS = 512;                         // 2 x 256 fp32 accumulators
+constexpr int TC_TMEM_COLS = 512;  // 2 x 256 fp32 accumulators
 constexpr float LOG2E = 1.4426950408889634f;
+
+// CG: CTAs per tile (cta_group). NB: 256-column accumulators per tile (1 =
+// 256-wide tile, TMEM double buffered; 2 = 512-wide tile filling all 512
+// TMEM columns, single buffered -- for the long-K dH/dW GEMMs whose
+// epilogue is rare, it halves the A re-reads).
+template <int CG, int NB>
+struct TcCfg {
+  static constexpr int A_BYTES = TC_BM * TC_BK * 2;            // 16 KB: this CTA's 128 rows
+  static constexpr int PART_ROWS = TC_BN / CG;                 // B rows per CTA per 256-col part
+  static constexpr int PART_BYTES = PART_ROWS * TC_BK * 2;     // 32 KB | 16 KB
+  static constexpr int B_BYTES = NB * PART_BYTES;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;        // 48 KB | 32 KB | 48 KB
+  static constexpr int STAGES = (200 * 1024) / STAGE_BYTES;    // 4 | 6 | 4
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int TILE_M = TC_BM * CG;
+  static constexpr int TILE_N = TC_BN * NB;
+  static constexpr int ACC_STAGES = NB == 1 ? 2 : 1;
+};
 
 enum { EPI_LSE = 0, EPI_DZ = 1, EPI_ROWS = 2, EPI_ACC = 3 };
 
@@ -47,6 +69,7 @@ struct TcArgs {
   int32_t n_tiles;
   int32_t m_dyn, k_dyn;
   int32_t group_m;
+  int32_t l2_policy;   // TMA L2 hint: 0 normal, 1 evict_last, 2 evict_first
   const WsHeader* hdr;
   float inv_temp;
   int32_t vocab;
@@ -84,80 +107,100 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   return *reinterpret_cast<const uint32_t*>(&v);
 }
 
-template <int AMN, int BMN, int EPI>
+template <int CG, int NB, int AMN, int BMN, int EPI>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
           const TcArgs args) {
+  using C = TcCfg<CG, NB>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
   uint8_t* sA = smem;
-  uint8_t* sB = smem + TC_STAGES * TC_A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + TC_STAGES * TC_STAGE_BYTES);
-  uint64_t* empty = full + TC_STAGES;
-  uint64_t* tfull = empty + TC_STAGES;
+  uint8_t* sB = smem + C::STAGES * C::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
+  const bool leader = rank == 0;
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
-    for (int i = 0; i < TC_STAGES; ++i) {
-      mbar_init(full + i, 1);
-      mbar_init(empty + i, 1);
+    for (int i = 0; i < C::STAGES; ++i) {
+      mbar_init(full + i, CG);     // CG producers arrive (remote for the peer)
+      mbar_init(empty + i, 1);     // one (multicast) commit per phase
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(tfull + i, 1);
-      mbar_init(tempty + i, 128);
+      mbar_init(tempty + i, 128 * CG);  // all epilogue threads of the pair
     }
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, TC_TMEM_COLS);
+  if (warp == 1) {
+    if constexpr (CG == 2) tmem_alloc_2sm(tmem_slot, TC_TMEM_COLS);
+    else tmem_alloc(tmem_slot, TC_TMEM_COLS);
+  }
   tc_fence_before();
-  __syncthreads();
+  __syncwarp();
+  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   const int64_t T = args.hdr->n_active;
   const int64_t M = args.m_dyn ? T : args.M;
   const int64_t K = args.k_dyn ? T : args.K;
-  const int64_t m_tiles = (M + TC_BM - 1) / TC_BM;
+  const int64_t m_tiles = (M + C::TILE_M - 1) / C::TILE_M;
   const int64_t num_k = (K + TC_BK - 1) / TC_BK;
   const int64_t num_tiles = num_k > 0 ? m_tiles * args.n_tiles : 0;
+  const int64_t cid = blockIdx.x / CG, ncl = gridDim.x / CG;
 
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------------ TMA producer
-      const uint64_t pol_a = l2_policy_evict_last();
-      const uint64_t pol_b = l2_policy_evict_last();
+      const uint64_t pol = args.l2_policy == 1   ? l2_policy_evict_last()
+                           : args.l2_policy == 2 ? l2_policy_evict_first()
+                                                 : l2_policy_evict_normal();
       int stage = 0;
       uint32_t phase = 0;
-      for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      for (int64_t tile = cid; tile < num_tiles; tile += ncl) {
         int64_t mb;
         int nb;
         tile_coords(tile, m_tiles, args.n_tiles, args.group_m, mb, nb);
-        const int32_t m0 = static_cast<int32_t>(mb * TC_BM), n0 = nb * TC_BN;
+        const int32_t m0 = static_cast<int32_t>(mb * C::TILE_M + rank * TC_BM);
+        // part p of this CTA's B: global rows n0 + p*256 + [0, PART_ROWS)
+        const int32_t n0 = nb * C::TILE_N + static_cast<int32_t>(rank) * C::PART_ROWS;
         for (int64_t kb = 0; kb < num_k; ++kb) {
           mbar_wait(empty + stage, phase ^ 1);
-          mbar_arrive_expect_tx(full + stage, TC_STAGE_BYTES);
-          uint8_t* a_dst = sA + stage * TC_A_BYTES;
-          uint8_t* b_dst = sB + stage * TC_B_BYTES;
+          if (leader) mbar_arrive_expect_tx(full + stage, C::STAGE_BYTES * CG);
+          else mbar_arrive_cluster(full + stage, 0);
+          uint8_t* a_dst = sA + stage * C::A_BYTES;
+          uint8_t* b_dst = sB + stage * C::B_BYTES;
           const int32_t k0 = static_cast<int32_t>(kb * TC_BK);
+          auto load = [&](const CUtensorMap* m, void* dst, int32_t c0, int32_t c1) {
+            if constexpr (CG == 2) tma_load_2d_2sm(m, full + stage, dst, c0, c1, pol);
+            else tma_load_2d(m, full + stage, dst, c0, c1, pol);
+          };
           if (AMN) {
-            tma_load_2d(&tmA, full + stage, a_dst, m0, k0, pol_a);
-            tma_load_2d(&tmA, full + stage, a_dst + 8192, m0 + 64, k0, pol_a);
+            load(&tmA, a_dst, m0, k0);
+            load(&tmA, a_dst + 8192, m0 + 64, k0);
           } else {
-            tma_load_2d(&tmA, full + stage, a_dst, k0, m0, pol_a);
+            load(&tmA, a_dst, k0, m0);
           }
-          if (BMN) {
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
-              tma_load_2d(&tmB, full + stage, b_dst + i * 8192, n0 + 64 * i, k0, pol_b);
-          } else {
-            tma_load_2d(&tmB, full + stage, b_dst, k0, n0, pol_b);
+          for (int p = 0; p < NB; ++p) {
+            uint8_t* pd = b_dst + p * C::PART_BYTES;
+            const int32_t np = n0 + p * TC_BN;
+            if (BMN) {
+#pragma unroll
+              for (int i = 0; i < C::PART_ROWS / 64; ++i) load(&tmB, pd + i * 8192, np + 64 * i, k0);
+            } else {
+              load(&tmB, pd, k0, np);
+            }
           }
-          if (++stage == TC_STAGES) {
+          if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
           }
@@ -165,55 +208,72 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    if (lane == 0 && leader) {
       // ------------------------------------------------------- MMA issuer
-      constexpr uint32_t IDESC = umma_idesc_bf16(TC_BM, TC_BN, AMN, BMN);
+      constexpr uint32_t IDESC = umma_idesc_bf16(TC_BM * CG, TC_BN, AMN, BMN);
       const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      for (int64_t tile = cid; tile < num_tiles; tile += ncl) {
         mbar_wait(tempty + acc, acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * TC_BN);
         for (int64_t kb = 0; kb < num_k; ++kb) {
           mbar_wait(full + stage, phase);
           tc_fence_after();
-          const uint32_t a_addr = a_base + stage * TC_A_BYTES;
-          const uint32_t b_addr = b_base + stage * TC_B_BYTES;
+          const uint32_t a_addr = a_base + stage * C::A_BYTES;
+          const uint32_t b_addr = b_base + stage * C::B_BYTES;
 #pragma unroll
           for (int k = 0; k < TC_BK / 16; ++k) {
             const uint64_t ad = AMN ? umma_desc_sw128(a_addr + k * 2048, 8192, 1024)
                                     : umma_desc_sw128(a_addr + k * 32, 0, 1024);
-            const uint64_t bd = BMN ? umma_desc_sw128(b_addr + k * 2048, 8192, 1024)
-                                    : umma_desc_sw128(b_addr + k * 32, 0, 1024);
-            tc_mma_f16(d_tmem, ad, bd, IDESC, (kb > 0 || k > 0) ? 1u : 0u);
+            const uint32_t accum = (kb > 0 || k > 0) ? 1u : 0u;
+#pragma unroll
+            for (int p = 0; p < NB; ++p) {
+              const uint32_t bp = b_addr + p * C::PART_BYTES;
+              const uint64_t bd = BMN ? umma_desc_sw128(bp + k * 2048, 8192, 1024)
+                                      : umma_desc_sw128(bp + k * 32, 0, 1024);
+              if constexpr (CG == 2) tc_mma_f16_2sm(d_tmem + p * TC_BN, ad, bd, IDESC, accum);
+              else tc_mma_f16(d_tmem + p * TC_BN, ad, bd, IDESC, accum);
+            }
           }
-          tc_commit(empty + stage);
-          if (++stage == TC_STAGES) {
+          if constexpr (CG == 2) tc_commit_2sm(empty + stage); else tc_commit(empty + stage);
+          if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        tc_commit(tfull + acc);
-        acc ^= 1;
-        if (acc == 0) acc_phase ^= 1;
+        if constexpr (CG == 2) tc_commit_2sm(tfull + acc); else tc_commit(tfull + acc);
+        if (++acc == C::ACC_STAGES) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
       }
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
     const int ew = warp - 4;
-    const int rit = ew * 32 + lane;  // row in tile == TMEM lane
+    const int rit = ew * 32 + lane;  // row in this CTA's half tile == TMEM lane
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+    auto release = [&](int a) {
+      tc_fence_before();
+      if constexpr (CG == 2) {
+        if (leader) mbar_arrive(tempty + a); else mbar_arrive_cluster(tempty + a, 0);
+      } else {
+        mbar_arrive(tempty + a);
+      }
+    };
+    for (int64_t tile = cid; tile < num_tiles; tile += ncl) {
       int64_t mb;
       int nb;
       tile_coords(tile, m_tiles, args.n_tiles, args.group_m, mb, nb);
-      const int64_t row = mb * TC_BM + rit;
-      const int n0 = nb * TC_BN;
+      const int64_t row = mb * C::TILE_M + rank * TC_BM + rit;
+      const int n0 = nb * C::TILE_N;
       const bool row_ok = row < M;
+      static_assert(NB == 1 || EPI == EPI_ROWS || EPI == EPI_ACC, "512-wide tiles: dH/dW only");
       mbar_wait(tfull + acc, acc_phase);
       tc_fence_after();
       const uint32_t taddr =
@@ -266,8 +326,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             }
           }
         }
-        tc_fence_before();
-        mbar_arrive(tempty + acc);
+        release(acc);
         if (row_ok) {
           const int64_t o = static_cast<int64_t>(nb) * args.ldp + row;
           args.pm[o] = m;
@@ -286,6 +345,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           uint32_t v[32];
           tmem_ld_32x32b_x32(taddr + c * 32, v);
           tmem_ld_wait();
+          if (c == TC_BN / 32 - 1) release(acc);
           uint32_t pk[16];
 #pragma unroll
           for (int j = 0; j < 32; j += 2) {
@@ -299,16 +359,15 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           for (int q = 0; q < 4; ++q)
             dst[c * 4 + q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
         }
-        tc_fence_before();
-        mbar_arrive(tempty + acc);
       } else if constexpr (EPI == EPI_ROWS) {
         const int64_t orow = row_ok ? static_cast<int64_t>(args.row_idx[row]) : 0;
         uint4* dst = reinterpret_cast<uint4*>(args.out + orow * args.ld_out + n0);
 #pragma unroll 1
-        for (int c = 0; c < TC_BN / 32; ++c) {
+        for (int c = 0; c < C::TILE_N / 32; ++c) {
           uint32_t v[32];
           tmem_ld_32x32b_x32(taddr + c * 32, v);
           tmem_ld_wait();
+          if (c == C::TILE_N / 32 - 1) release(acc);
           if (row_ok && n0 + c * 32 < args.N) {
             uint32_t pk[16];
 #pragma unroll
@@ -319,15 +378,14 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
               dst[c * 4 + q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
           }
         }
-        tc_fence_before();
-        mbar_arrive(tempty + acc);
       } else {  // EPI_ACC
         float4* dst = reinterpret_cast<float4*>(args.acc + row * args.ld_acc + n0);
 #pragma unroll 1
-        for (int c = 0; c < TC_BN / 32; ++c) {
+        for (int c = 0; c < C::TILE_N / 32; ++c) {
           uint32_t v[32];
           tmem_ld_32x32b_x32(taddr + c * 32, v);
           tmem_ld_wait();
+          if (c == C::TILE_N / 32 - 1) release(acc);
           if (row_ok && n0 + c * 32 < args.N) {
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
@@ -340,18 +398,21 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             }
           }
         }
-        tc_fence_before();
-        mbar_arrive(tempty + acc);
       }
-      acc ^= 1;
-      if (acc == 0) acc_phase ^= 1;
+      if (++acc == C::ACC_STAGES) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
     }
   }
-  __syncthreads();
+  tc_fence_before();
+  __syncwarp();
+  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
   if (warp == 1) {
     __syncwarp();
     tc_fence_after();
-    tmem_dealloc(tmem_base, TC_TMEM_COLS);
+    if constexpr (CG == 2) tmem_dealloc_2sm(tmem_base, TC_TMEM_COLS);
+    else tmem_dealloc(tmem_base, TC_TMEM_COLS);
   }
 }
 
@@ -404,23 +465,83 @@ int num_sms() {
   return n;
 }
 
-template <int AMN, int BMN, int EPI>
+// Tuning knobs read once from the environment (benchmarks / A-B tests).
+static int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return (e && *e) ? std::atoi(e) : dflt;
+}
+
+// CTA group of the tensor-core GEMMs: 2 (default) or 1 (RLHEAD_CTA_GROUP=1).
+int tc_cta_group() {
+  static int cg = 0;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* e = std::getenv("RLHEAD_CTA_GROUP");
+    cg = (e && e[0] == '1') ? 1 : 2;
+  });
+  return cg;
+}
+
+template <int CG, int NB, int AMN, int BMN, int EPI>
 static rl_status run_gemm(const CUtensorMap& a, const CUtensorMap& b, const TcArgs& args,
-                          int64_t tiles_bound, int kind, cudaStream_t s) {
+                          int64_t m_extent, int kind, cudaStream_t s) {
+  using C = TcCfg<CG, NB>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(k_tc_gemm<AMN, BMN, EPI>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_BYTES);
+    attr_err = cudaFuncSetAttribute(k_tc_gemm<CG, NB, AMN, BMN, EPI>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
   });
   if (attr_err != cudaSuccess) return RL_ERR_CUDA;
+  const int64_t tiles_bound = ceil_div(m_extent, C::TILE_M) * args.n_tiles;
   if (tiles_bound <= 0) return RL_OK;
-  const int64_t grid = tiles_bound < num_sms() ? tiles_bound : num_sms();
+  const int64_t clusters_max = num_sms() / CG;
+  const int64_t clusters = tiles_bound < clusters_max ? tiles_bound : clusters_max;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(clusters * CG));
+  cfg.blockDim = dim3(TC_THREADS);
+  cfg.dynamicSmemBytes = C::SMEM_BYTES;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
   TraceScope ts(kind, s);
-  k_tc_gemm<AMN, BMN, EPI><<<static_cast<unsigned>(grid), TC_THREADS, TC_SMEM_BYTES, s>>>(a, b,
-                                                                                          args);
+  if (cudaLaunchKernelEx(&cfg, k_tc_gemm<CG, NB, AMN, BMN, EPI>, a, b, args) != cudaSuccess)
+    return RL_ERR_CUDA;
   RLH_CHECK_LAUNCH();
   return RL_OK;
+}
+
+// 256-wide tiles (double-buffered TMEM) for the short-K forward/dZ GEMMs.
+template <int AMN, int BMN, int EPI>
+static rl_status run_narrow(const CUtensorMap& a, const CUtensorMap& b, TcArgs t,
+                            int64_t m_extent, int kind, cudaStream_t s) {
+  t.n_tiles = static_cast<int32_t>(ceil_div(t.N, TC_BN));
+  t.group_m = env_int("RLHEAD_GROUP_M", 32) / tc_cta_group();
+  if (t.group_m < 1) t.group_m = 1;
+  if (tc_cta_group() == 2) return run_gemm<2, 1, AMN, BMN, EPI>(a, b, t, m_extent, kind, s);
+  return run_gemm<1, 1, AMN, BMN, EPI>(a, b, t, m_extent, kind, s);
+}
+
+// Long-K dH/dW GEMMs: 256 x 512 pair tiles (all 512 TMEM columns), rastered
+// N-fastest so the CTA pairs sharing an A panel run together.
+static bool wide_bwd() { return tc_cta_group() == 2 && env_int("RLHEAD_WIDE", 1) != 0; }
+template <int AMN, int BMN, int EPI>
+static rl_status run_wide(const CUtensorMap& a, const CUtensorMap& b, TcArgs t, int64_t m_extent,
+                          int kind, cudaStream_t s) {
+  t.group_m = env_int("RLHEAD_GROUP_M_BWD", 1);
+  if (t.group_m < 1) t.group_m = 1;
+  if (wide_bwd()) {
+    t.n_tiles = static_cast<int32_t>(ceil_div(t.N, 2 * TC_BN));
+    return run_gemm<2, 2, AMN, BMN, EPI>(a, b, t, m_extent, kind, s);
+  }
+  t.n_tiles = static_cast<int32_t>(ceil_div(t.N, TC_BN));
+  if (tc_cta_group() == 2) return run_gemm<2, 1, AMN, BMN, EPI>(a, b, t, m_extent, kind, s);
+  return run_gemm<1, 1, AMN, BMN, EPI>(a, b, t, m_extent, kind, s);
 }
 
 static TcArgs base_args(const rl_head* hd, const WsLayout& L, char* ws) {
@@ -428,7 +549,7 @@ static TcArgs base_args(const rl_head* hd, const WsLayout& L, char* ws) {
   t.hdr = reinterpret_cast<const WsHeader*>(ws + L.off_hdr);
   t.inv_temp = hd->inv_temperature;
   t.vocab = hd->vocab;
-  t.group_m = 16;
+  t.l2_policy = env_int("RLHEAD_L2_POLICY", 1);
   t.tgt_c = reinterpret_cast<const int32_t*>(ws + L.off_tgt);
   t.ldp = L.Rp;
   return t;
@@ -437,46 +558,45 @@ static TcArgs base_args(const rl_head* hd, const WsLayout& L, char* ws) {
 rl_status launch_tc_fwd(const rl_head* hd, const void* weight, const WsLayout& L, char* ws,
                         cudaStream_t s) {
   const int h = hd->hidden, V = hd->vocab;
+  const int cg = tc_cta_group();
   CUtensorMap ma, mb;
   if (!make_map(&ma, ws + L.off_hc, h, L.Rp, static_cast<uint64_t>(h) * 2, TC_BM) ||
-      !make_map(&mb, weight, h, V, static_cast<uint64_t>(h) * 2, TC_BN))
+      !make_map(&mb, weight, h, V, static_cast<uint64_t>(h) * 2, TC_BN / cg))
     return RL_ERR_CUDA;
   TcArgs t = base_args(hd, L, ws);
   t.M = L.Rp;
   t.m_dyn = 1;
   t.K = h;
   t.N = V;
-  t.n_tiles = static_cast<int32_t>(L.n_vt);
   t.pm = reinterpret_cast<float*>(ws + L.off_pm);
   t.ps = reinterpret_cast<float*>(ws + L.off_ps);
   t.pu = reinterpret_cast<float*>(ws + L.off_pu);
   t.zy = reinterpret_cast<float*>(ws + L.off_zy);
-  return run_gemm<0, 0, EPI_LSE>(ma, mb, t, (L.Rp / TC_BM) * L.n_vt, RL_K_GEMM_LSE, s);
+  return run_narrow<0, 0, EPI_LSE>(ma, mb, t, L.Rp, RL_K_GEMM_LSE, s);
 }
 
 rl_status launch_tc_bwd(const rl_head* hd, const void* weight, void* grad_hidden,
                         float* grad_weight, const WsLayout& L, char* ws, cudaStream_t s) {
   const int h = hd->hidden, V = hd->vocab;
-  const int h_tiles = static_cast<int>(ceil_div(h, TC_BN));
+  const int cg = tc_cta_group();
   __nv_bfloat16* dz = reinterpret_cast<__nv_bfloat16*>(ws + L.off_dz);
   rl_status st;
   // N5: recompute logits, dZ = tau^-1 g (onehot - p) -> bf16 [Rp, Vp].
   {
     CUtensorMap ma, mb;
     if (!make_map(&ma, ws + L.off_hc, h, L.Rp, static_cast<uint64_t>(h) * 2, TC_BM) ||
-        !make_map(&mb, weight, h, V, static_cast<uint64_t>(h) * 2, TC_BN))
+        !make_map(&mb, weight, h, V, static_cast<uint64_t>(h) * 2, TC_BN / cg))
       return RL_ERR_CUDA;
     TcArgs t = base_args(hd, L, ws);
     t.M = L.Rp;
     t.m_dyn = 1;
     t.K = h;
     t.N = V;
-    t.n_tiles = static_cast<int32_t>(L.n_vt);
     t.lse_c = reinterpret_cast<const float*>(ws + L.off_lse);
     t.g_c = reinterpret_cast<const float*>(ws + L.off_g);
     t.dz = dz;
     t.ld_dz = L.Vp;
-    st = run_gemm<0, 0, EPI_DZ>(ma, mb, t, (L.Rp / TC_BM) * L.n_vt, RL_K_GEMM_DZ, s);
+    st = run_narrow<0, 0, EPI_DZ>(ma, mb, t, L.Rp, RL_K_GEMM_DZ, s);
     if (st != RL_OK) return st;
   }
   // N6: dH[T, h] = dZ[T, V] W[V, h]; rows -> grad_hidden[active_idx[r]].
@@ -490,11 +610,10 @@ rl_status launch_tc_bwd(const rl_head* hd, const void* weight, void* grad_hidden
     t.m_dyn = 1;
     t.K = V;
     t.N = h;
-    t.n_tiles = h_tiles;
     t.out = static_cast<__nv_bfloat16*>(grad_hidden);
     t.ld_out = hd->ld_hidden;
     t.row_idx = reinterpret_cast<const int32_t*>(ws + L.off_active);
-    st = run_gemm<0, 1, EPI_ROWS>(ma, mb, t, (L.Rp / TC_BM) * h_tiles, RL_K_GEMM_DH, s);
+    st = run_wide<0, 1, EPI_ROWS>(ma, mb, t, L.Rp, RL_K_GEMM_DH, s);
     if (st != RL_OK) return st;
   }
   // N7: dW[V, h] += dZ^T[V, T] Hc[T, h].
@@ -508,10 +627,9 @@ rl_status launch_tc_bwd(const rl_head* hd, const void* weight, void* grad_hidden
     t.K = L.Rp;
     t.k_dyn = 1;
     t.N = h;
-    t.n_tiles = h_tiles;
     t.acc = grad_weight;
     t.ld_acc = h;
-    st = run_gemm<1, 1, EPI_ACC>(ma, mb, t, ceil_div(V, TC_BM) * h_tiles, RL_K_GEMM_DW, s);
+    st = run_wide<1, 1, EPI_ACC>(ma, mb, t, V, RL_K_GEMM_DW, s);
     if (st != RL_OK) return st;
   }
   return RL_OK;

@@ -1,0 +1,78 @@
+#!/usr/bin/env python
+"""Quick GEMM probe: one micro-batch of a config through rl_policy_loss_fwd_bwd
+`--reps` times, per-kernel-kind device times (library CUDA-event tracer).
+Cheap to set up (only the micro-batch's rows are generated), so it is the
+command to wrap in ncu for kernel experiments:
+
+    python scripts/probe.py --config qwen7b --reps 3
+    ncu --metrics ... -k regex:k_tc_gemm python scripts/probe.py --reps 1
+"""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="qwen7b")
+    ap.add_argument("--rows", type=int, default=65536)
+    ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--fwd-only", action="store_true")
+    a = ap.parse_args()
+    import torch
+
+    import paper_2509_15965_b200 as rl
+    from paper_2509_15965_b200.dp import pack_micro_batches
+    from workload import CONFIGS, make_layout, make_tensors_torch, sub_layout
+    cfg = CONFIGS[a.config]
+    lay = make_layout(cfg, 0)
+    cu = lay.cu_seqlens.astype(np.int64)
+    s0, s1 = pack_micro_batches(cu[1:] - cu[:-1], a.rows)[0]
+    mb, _ = sub_layout(lay, np.arange(s0, s1))
+    dev = "cuda"
+    H, W = make_tensors_torch(cfg, mb.num_rows, seed=0, device=dev)
+    head = rl.Head(cfg.hidden, cfg.vocab, cfg.dtype)
+    b = rl.Batch(torch.as_tensor(mb.cu_seqlens, device=dev), torch.as_tensor(mb.targets, device=dev),
+                 torch.as_tensor(mb.mask, device=dev))
+    R = mb.num_rows
+    old = torch.zeros(R, device=dev)
+    adv = torch.linspace(-1, 1, mb.num_seqs, device=dev)
+    p = rl.LossParams(n_tokens_global=torch.tensor([lay.num_tokens], device=dev))
+    logp = torch.empty(R, device=dev)
+    gh = torch.empty_like(H)
+    gw = torch.zeros(cfg.vocab, cfg.hidden, device=dev)
+    ws = rl.Workspace(dev)
+    tr = rl.Trace(4096)
+
+    def once():
+        if a.fwd_only:
+            rl.rl_logprob_fwd(head, H, W, b, logp, ws=ws)
+        else:
+            rl.rl_policy_loss_fwd_bwd(head, H, W, b, old, adv, p, logp, gh, gw, ws=ws)
+
+    once()
+    torch.cuda.synchronize()
+    tr.start()
+    for _ in range(a.reps):
+        once()
+    torch.cuda.synchronize()
+    tr.stop()
+    tok = int(mb.mask.sum())
+    out = {"config": a.config, "tokens": tok, "reps": a.reps}
+    for k, (c, t) in tr.by_kind().items():
+        ms = t / c
+        entry = {"ms": round(ms, 3)}
+        if k.startswith("gemm"):
+            entry["tflops"] = round(2.0 * cfg.hidden * cfg.vocab * tok / (ms / 1e3) / 1e12, 1)
+        out[k] = entry
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()

@@ -154,6 +154,14 @@ __host__ __device__ constexpr uint32_t umma_idesc_bf16(uint32_t M, uint32_t N, u
          ((N >> 3) << 17) | ((M >> 4) << 24);
 }
 
+// 16-B global store with an L2 eviction-priority policy (streaming outputs
+// that must not push the GEMM operand panels out of L2).
+__device__ __forceinline__ void st_global_v4_hint(void* p, uint4 v, uint64_t policy) {
+  asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "r"(v.x),
+               "r"(v.y), "r"(v.z), "r"(v.w), "l"(policy)
+               : "memory");
+}
+
 // ------------------------------------------------- clusters / CTA pairs ----
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;

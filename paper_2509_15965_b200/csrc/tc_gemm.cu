@@ -340,6 +340,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         const int yrel = (row_ok ? args.tgt_c[row] : -1) - n0;
         const float lse2 = lse * LOG2E, sc2 = args.inv_temp * LOG2E;
         uint4* dst = reinterpret_cast<uint4*>(args.dz + row * args.ld_dz + n0);
+        const uint64_t st_pol = l2_policy_evict_first();  // 17 GB stream: keep W/Hc in L2
 #pragma unroll 1
         for (int c = 0; c < TC_BN / 32; ++c) {
           uint32_t v[32];
@@ -357,7 +358,9 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           }
 #pragma unroll
           for (int q = 0; q < 4; ++q)
-            dst[c * 4 + q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+            st_global_v4_hint(dst + c * 4 + q,
+                              make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]),
+                              st_pol);
         }
       } else if constexpr (EPI == EPI_ROWS) {
         const int64_t orow = row_ok ? static_cast<int64_t>(args.row_idx[row]) : 0;

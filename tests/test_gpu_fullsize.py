@@ -60,9 +60,18 @@ def test_fullsize_sampled_rows(rl, name):
     inact = torch.as_tensor(mb.mask == 0, device=dev)
     assert gh[inact].abs().max().item() == 0 if inact.any() else True
     assert logp[inact].abs().max().item() == 0 if inact.any() else True
-    # P14 at full size: sum_j dW_j = 0 up to bf16 dZ rounding
-    colsum = gw.double().sum(0).abs().max().item()
-    assert colsum <= 1e-2 * gw.abs().max().item()
+    # P14 at full size: sum_j dW_j = sum_t (sum_j dZ_tj) h_t is 0 exactly; with
+    # dZ rounded to bf16 each row sum is bounded by 2^-8 * sum_j |dZ_tj|
+    # = 2^-8 * 2|g_t|(1 - p_y) <= 2^-7 |g_t|, so |colsum_k| <= 2^-7 sum_t |g_t h_tk|
+    # (g_t from this run's logp; a consistency bound, not an oracle value).
+    act_t = torch.as_tensor(mb.mask.astype(bool), device=dev)
+    seq_t = torch.as_tensor(np.searchsorted(mb.cu_seqlens, np.arange(R), side="right") - 1,
+                            device=dev)
+    r_t = torch.exp(torch.clamp(logp - old, -20, 20))
+    g_bound = (adv[seq_t].abs() * r_t / N * act_t).double()
+    colsum = gw.double().sum(0).abs()
+    bound = 2.0 ** -7 * (g_bound[:, None] * H.double().abs()).sum(0) * 1.05 + 1e-12
+    assert bool((colsum <= bound).all()), float((colsum / bound).max())
     # sampled rows vs oracle (exact fp64 on the device tensors' values)
     rng = np.random.default_rng(0)
     act = np.flatnonzero(mb.mask)

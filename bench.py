@@ -46,7 +46,7 @@ def parse():
     p.add_argument("--max-mb", type=int, default=0, help="debug: first micro-batches only")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--cpu-sample-tokens", type=int, default=96)
+    p.add_argument("--cpu-sample-tokens", type=int, default=512)
     return p.parse_args()
 
 

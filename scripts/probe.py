@@ -24,6 +24,8 @@ def main():
     ap.add_argument("--rows", type=int, default=65536)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--fwd-only", action="store_true")
+    ap.add_argument("--cublas", action="store_true", help="also time torch.matmul of the shapes")
+    ap.add_argument("--sustain", type=float, default=0.0, help="seconds of warm-up load")
     a = ap.parse_args()
     import torch
 
@@ -58,13 +60,40 @@ def main():
 
     once()
     torch.cuda.synchronize()
+    import time
+    t_end = time.time() + a.sustain
+    while time.time() < t_end:         # reach the power-capped steady state
+        once()
+        torch.cuda.synchronize()
+    tok = int(mb.mask.sum())
+    out = {"config": a.config, "tokens": tok, "reps": a.reps}
+    shapes = {}
+    if a.cublas:
+        # library reference: cuBLAS (torch.matmul) for the same GEMM shapes,
+        # outputs materialised (what an unfused head would do); timed
+        # interleaved with ours so both see the same power/clock state.
+        Hc = H[torch.as_tensor(np.flatnonzero(mb.mask), device=dev)].contiguous()
+        shapes = {"cublas_fwd_HWt": (Hc, W.t()),
+                  "cublas_dH_ZW": (torch.empty(tok, cfg.vocab, dtype=H.dtype, device=dev), W),
+                  "cublas_dW_ZtH": (torch.empty(cfg.vocab, tok, dtype=H.dtype, device=dev), Hc)}
+    cub = {k: 0.0 for k in shapes}
     tr.start()
     for _ in range(a.reps):
         once()
+        for k, (x, y) in shapes.items():
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            z = torch.matmul(x, y)
+            e1.record()
+            torch.cuda.synchronize()
+            cub[k] += e0.elapsed_time(e1)
+            del z
     torch.cuda.synchronize()
     tr.stop()
-    tok = int(mb.mask.sum())
-    out = {"config": a.config, "tokens": tok, "reps": a.reps}
+    for k, t in cub.items():
+        ms = t / a.reps
+        out[k] = {"ms": round(ms, 3),
+                  "tflops": round(2.0 * cfg.hidden * cfg.vocab * tok / (ms / 1e3) / 1e12, 1)}
     for k, (c, t) in tr.by_kind().items():
         ms = t / c
         entry = {"ms": round(ms, 3)}

@@ -240,13 +240,28 @@ def grpo_advantage_from_stats(rewards, group_of_seq, sum_stats, max_stats, eps=1
 #   act = not((A > 0 and r > 1+eps_hi) or (A < 0 and r < 1-eps_lo)).
 # Backward through softmax: dz = tau^-1 g (onehot(y) - p); dH = dz W;
 # dW = sum_t dz_t^T h_t (BASELINE.json north_star: "dL/dhidden and dL/dW").
+#
+# NEXT-1 variants (DESIGN.md §3 #25-#28; the algorithms the paper cites,
+# PPO/DAPO/GRPO P:L184; all off by default):
+#   dual clip (A < 0): l = min(max(-A r, -A clip(r)), -A c_dual), grad 0 if r > c_dual;
+#   KL to a reference policy, k3 estimator: k = e^{q} - q - 1, q = clamp(ref - logp),
+#     dk/dlogp = 1 - e^{q} (0 if clamped);
+#   entropy bonus: - c_ent H_t, dH_t/dz_j = -p_j (z_j - E_p[z]);
+#   aggregation: token mean (w_t = 1/N) or seq-mean-token-mean
+#     (w_t = 1 / (S n_s), n_s = active tokens of t's sequence, S = sequences
+#     with n_s >= 1 over the mini-batch).
+#   L = sum_t m_t w_t (l_t + beta k_t - c_ent H_t).
 # --------------------------------------------------------------------------
 @dataclass
 class LossParams:
     clip_lo: float = 0.2
     clip_hi: float = 0.2
     logratio_clamp: float = 20.0
-    loss_scale: float | None = None     # None -> 1 / n_global
+    loss_scale: float | None = None     # None -> 1 / n_global (token mean)
+    dual_clip: float = 0.0              # c_dual > 1 enables dual clip for A < 0
+    kl_coef: float = 0.0                # beta
+    entropy_coef: float = 0.0           # c_ent
+    seq_mean: bool = False              # seq-mean-token-mean aggregation
 
 
 def _surrogate(logp, old, A, p: LossParams):
@@ -259,25 +274,40 @@ def _surrogate(logp, old, A, p: LossParams):
     clipped_hi = A > 0 and r > hi
     clipped_lo = A < 0 and r < lo
     act = not (clipped_hi or clipped_lo)
+    if p.dual_clip > 0 and A < 0:
+        loss = min(loss, -A * p.dual_clip)
+        if r > p.dual_clip:
+            act = False
     inrange = abs(d) <= c
     dl_dlogp = (-A * r) if (act and inrange) else 0.0
     return r, loss, dl_dlogp, clipped_lo, clipped_hi
 
 
+def _kl_k3(logp, ref, c):
+    """k3 estimator of KL(pi || ref) at one token and its d/dlogp."""
+    q0 = ref - logp
+    q = min(max(q0, -c), c)
+    k = math.exp(q) - q - 1.0
+    dk = (1.0 - math.exp(q)) if abs(q0) <= c else 0.0
+    return k, dk
+
+
 def policy_loss_fwd_bwd(hidden, weight, cu_seqlens, mask, targets, old_logp, adv_seq,
                         params: LossParams | None = None, n_global=None,
-                        inv_temperature=1.0, want_grads=True):
-    """Forward + backward of the masked clipped-ratio token-mean loss.
+                        inv_temperature=1.0, want_grads=True, ref_logp=None, n_seqs_global=None):
+    """Forward + backward of the masked clipped-ratio loss (token mean by default).
 
     hidden [R, h]; weight [V, h]; old_logp [R]; adv_seq [S] (one advantage per
     sequence, broadcast to its rows). n_global = the loss normaliser N (masked
     tokens of the whole mini-batch over all ranks, reading #13); defaults to
-    this batch's active count. loss_scale, when given, replaces 1/N.
+    this batch's active count. loss_scale, when given, replaces 1/N (and
+    1/S under seq_mean). ref_logp [R] is needed when kl_coef > 0;
+    n_seqs_global = S for seq_mean (default: this batch's non-empty sequences).
 
-    Returns dict(loss, loss_sum, logp, entropy, lse, g, dH [R,h], dW [V,h],
-    stats{loss_sum, ratio_sum, entropy_sum, ratio_max, clip_lo_count,
-    clip_hi_count, tokens}, err). Inactive rows: logp = entropy = lse = g = 0
-    and dH row = 0.
+    Returns dict(loss, loss_sum, logp, entropy, lse, g, ge, dH [R,h], dW [V,h],
+    stats{loss_sum, ratio_sum, entropy_sum, kl_sum, objective, ratio_max,
+    clip_lo_count, clip_hi_count, tokens}, err). Inactive rows: logp = entropy
+    = lse = g = 0 and dH row = 0.
     """
     p = params or LossParams()
     W = _as64(weight)
@@ -287,16 +317,31 @@ def policy_loss_fwd_bwd(hidden, weight, cu_seqlens, mask, targets, old_logp, adv
     targets = np.asarray(targets).reshape(-1).astype(np.int64)
     old = _as64(old_logp).reshape(-1)
     adv = _as64(adv_seq).reshape(-1)
+    ref = None if ref_logp is None else _as64(ref_logp).reshape(-1)
+    if p.kl_coef > 0 and ref is None:
+        raise ValueError("kl_coef > 0 needs ref_logp")
     N = bk["n_active"] if n_global is None else int(n_global)
-    scale = (1.0 / N if N > 0 else 0.0) if p.loss_scale is None else float(p.loss_scale)
+    # per-token weights w_t
+    S_count = np.bincount(bk["row_seq"][bk["active"]], minlength=max(len(adv), 1))
+    if p.seq_mean:
+        S = int((S_count > 0).sum()) if n_seqs_global is None else int(n_seqs_global)
+        base = (1.0 / S if S > 0 else 0.0) if p.loss_scale is None else float(p.loss_scale)
+    else:
+        base = (1.0 / N if N > 0 else 0.0) if p.loss_scale is None else float(p.loss_scale)
+
+    def weight_of(t):
+        if p.seq_mean:
+            return base / S_count[bk["row_seq"][t]]
+        return base
 
     logp = np.zeros(R)
     ent = np.zeros(R)
     lse = np.zeros(R)
     g = np.zeros(R)
+    ge = np.zeros(R)
     dH = np.zeros((R, h)) if want_grads else None
     dW = np.zeros((V, h)) if want_grads else None
-    losses, ratios, ents = [], [], []
+    losses, ratios, ents, kls, objs = [], [], [], [], []
     ratio_max = 0.0
     n_lo = n_hi = 0
     act_rows = bk["active_idx"].astype(np.int64)
@@ -306,28 +351,39 @@ def policy_loss_fwd_bwd(hidden, weight, cu_seqlens, mask, targets, old_logp, adv
         Z, P, l, lp, e = _row_softmax_stats(Hc, W, targets[idx], inv_temperature)
         logp[idx], ent[idx], lse[idx] = lp, e, l
         gc = np.zeros(len(idx))
+        gec = np.zeros(len(idx))
         for j, t in enumerate(idx):
             A = float(adv[bk["row_seq"][t]])
             r, loss, dldlp, clo, chi = _surrogate(float(lp[j]), float(old[t]), A, p)
+            k, dk = (0.0, 0.0) if ref is None else _kl_k3(float(lp[j]), float(ref[t]),
+                                                            p.logratio_clamp)
+            w = weight_of(t)
             losses.append(loss)
             ratios.append(r)
             ents.append(float(e[j]))
+            kls.append(k)
+            objs.append(w * (loss + p.kl_coef * k - p.entropy_coef * float(e[j])))
             ratio_max = max(ratio_max, r)
             n_lo += int(clo)
             n_hi += int(chi)
-            gc[j] = scale * dldlp
+            gc[j] = w * (dldlp + p.kl_coef * dk)
+            gec[j] = w * p.entropy_coef
         g[idx] = gc
+        ge[idx] = gec
         if want_grads:
             onehot = np.zeros_like(P)
             onehot[np.arange(len(idx)), targets[idx]] = 1.0
-            dZ = inv_temperature * gc[:, None] * (onehot - P)
+            Ez = (P * Z).sum(axis=1, keepdims=True)
+            # d(-c H)/dz = +c p (z - E_p z)
+            dZ = inv_temperature * (gc[:, None] * (onehot - P) + gec[:, None] * P * (Z - Ez))
             dH[idx] = dZ @ W
             dW += dZ.T @ Hc
     loss_sum = math.fsum(losses)
+    objective = math.fsum(objs)
     stats = dict(loss_sum=loss_sum, ratio_sum=math.fsum(ratios), entropy_sum=math.fsum(ents),
-                 ratio_max=ratio_max, clip_lo_count=n_lo, clip_hi_count=n_hi,
-                 tokens=len(act_rows))
-    loss = loss_sum * scale
-    return dict(loss=loss, loss_sum=loss_sum, logp=logp, entropy=ent, lse=lse, g=g,
+                 kl_sum=math.fsum(kls), objective=objective, ratio_max=ratio_max,
+                 clip_lo_count=n_lo, clip_hi_count=n_hi, tokens=len(act_rows))
+    return dict(loss=objective, loss_sum=loss_sum, logp=logp, entropy=ent, lse=lse, g=g, ge=ge,
                 dH=dH, dW=dW, stats=stats, err=bk["err"], active=bk["active"],
-                row_seq=bk["row_seq"], n_active=bk["n_active"])
+                row_seq=bk["row_seq"], n_active=bk["n_active"],
+                n_seqs=int((S_count > 0).sum()))

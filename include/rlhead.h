@@ -95,10 +95,13 @@ RL_API size_t rl_workspace_size(const rl_head *hd, int64_t num_rows, int32_t wan
  *   at and beyond n_active are left unspecified.
  * n_active (device int64, out, may be NULL): number of active rows.
  * n_accum (device int64, ACCUMULATED +=, may be NULL): for the loss
- *   normaliser N summed over micro-batches/ranks (DESIGN.md §3 #13). */
+ *   normaliser N summed over micro-batches/ranks (DESIGN.md §3 #13).
+ * nseq_accum (device int64, ACCUMULATED +=, may be NULL): sequences with at
+ *   least one active row -- the normaliser S of seq-mean aggregation. */
 RL_API rl_status rl_batch_prepare(const rl_head *hd, const rl_batch *b, int32_t *row_seq,
                            int32_t *active_idx, int64_t *n_active, int64_t *n_accum,
-                           void *ws, size_t ws_bytes, rl_stream_t stream);
+                           int64_t *nseq_accum, void *ws, size_t ws_bytes,
+                           rl_stream_t stream);
 
 /* Inference-worker call: per-row log-prob of the
  * target, entropy (nats) and log-sum-exp of tau^-1 H W^T over the full V.
@@ -130,25 +133,43 @@ RL_API rl_status rl_grpo_advantage(const float *rewards, const int32_t *group_of
                             const double *max_stats, float eps, int32_t unbiased, float *adv,
                             int32_t *err_flags, rl_stream_t stream);
 
-/* Clipped surrogate parameters (host struct; DESIGN.md §3 #12-#15). */
+/* Loss parameters (host struct; DESIGN.md §3 #12-#15, NEXT-1 variants
+ * #25-#28). Per active token t of sequence s with weight w_t:
+ *   L += w_t (l_t + kl_coef * k3_t - entropy_coef * H_t)
+ *   l_t  = max(-A r, -A clip(r, 1-clip_lo, 1+clip_hi)), and for A < 0 with
+ *          dual_clip > 1: min(l_t, -A dual_clip)  (gradient 0 if r > dual_clip)
+ *   k3_t = e^q - q - 1, q = clamp(ref_logp_t - logp_t, -c, c)
+ *   w_t  = 1/N (token mean)  or, if seq_mean != 0,
+ *          1/(S n_s) with n_s the active tokens of s (seq-mean-token-mean).
+ * 1/N (1/S) comes from n_tokens_global (n_seqs_global) when given, else
+ * loss_scale is used in its place (streaming mode). */
 typedef struct {
   float clip_lo;                  /* eps_lo: ratio clipped below at 1 - eps_lo (0.2) */
   float clip_hi;                  /* eps_hi: ratio clipped above at 1 + eps_hi (0.2) */
   float logratio_clamp;           /* c: d = logp - old clamped to [-c, c] (20)       */
-  double loss_scale;              /* multiplies dL/dlogp when n_tokens_global NULL   */
+  double loss_scale;              /* used when the device normaliser is NULL         */
   const int64_t *n_tokens_global; /* device: N (all micro-batches, all ranks);
                                      scale = 1/N (0 if N == 0)                      */
+  float dual_clip;                /* 0 = off, else > 1                               */
+  float kl_coef;                  /* beta >= 0; > 0 needs ref_logp                   */
+  float entropy_coef;             /* c_ent >= 0 (entropy bonus)                      */
+  int32_t seq_mean;               /* 0 token mean, 1 seq-mean-token-mean             */
+  const float *ref_logp;          /* [R] device: reference-policy log-probs          */
+  const int64_t *n_seqs_global;   /* device: S (seq_mean); see rl_batch_prepare      */
 } rl_loss_params;
 
 /* Loss statistics, device resident, ACCUMULATED (+=) by every call. The
  * caller zeroes it at the start of a mini-batch. Raw sums over active rows:
- * L = loss_sum * scale. clip_hi_count = #{A>0, r>1+eps_hi},
+ * loss_sum = sum l_t, kl_sum = sum k3_t, objective = sum w_t(l_t + beta k3_t
+ * - c_ent H_t) (this call's share of L). clip_hi_count = #{A>0, r>1+eps_hi},
  * clip_lo_count = #{A<0, r<1-eps_lo}; ratio_max feeds the minibatch
  * early-stop. */
 typedef struct {
   double loss_sum;
   double ratio_sum;
   double entropy_sum;
+  double kl_sum;
+  double objective;
   float ratio_max;
   int32_t reserved;
   int64_t clip_lo_count;
@@ -163,9 +184,9 @@ typedef struct {
  *   grad_hidden [R, ld_hidden] out, dtype of hidden, 0 on inactive rows,
  *   grad_weight [V, h] fp32 ACCUMULATED (+=): zero it once per mini-batch,
  *   stats (device, may be NULL) ACCUMULATED.
- * dL/dlogp_t = -scale * A r [unclipped] [|d| <= c]; dZ = tau^-1 g (onehot-p);
- * dH = dZ W; dW += dZ^T H. Logits are recomputed in the backward instead of
- * stored. */
+ * g_t = dL/dlogp_t = w_t(-A r [unclipped][|d| <= c] + beta (1 - e^q));
+ * dZ = tau^-1 (g (onehot - p) + w c_ent p (z - E_p z)); dH = dZ W;
+ * dW += dZ^T H. Logits are recomputed in the backward instead of stored. */
 RL_API rl_status rl_policy_loss_fwd_bwd(const rl_head *hd, const void *hidden, const void *weight,
                                  const rl_batch *b, const float *old_logp, const float *adv,
                                  const rl_loss_params *p, float *logp, float *entropy,

@@ -78,10 +78,12 @@ bool ws_layout(const rl_head* hd, int64_t R, int want_bwd, WsLayout* L) {
   L->off_zy = take(static_cast<size_t>(L->Rp) * 4);
   L->off_lse = take(static_cast<size_t>(L->Rp) * 4);
   L->off_g = take(static_cast<size_t>(L->Rp) * 4);
+  L->off_ge = take(static_cast<size_t>(L->Rp) * 4);
+  L->off_ez = take(static_cast<size_t>(L->Rp) * 4);
   L->off_dz = take(want_bwd ? (tc ? static_cast<size_t>(L->Rp) * L->Vp * 2
                                   : static_cast<size_t>(L->Rp) * V * 4)
                             : 0);
-  L->off_st_d = take(static_cast<size_t>(L->nblk_loss) * 3 * 8);
+  L->off_st_d = take(static_cast<size_t>(L->nblk_loss) * 5 * 8);
   L->off_st_f = take(static_cast<size_t>(L->nblk_loss) * 4);
   L->off_st_i = take(static_cast<size_t>(L->nblk_loss) * 3 * 8);
   L->total = o;
@@ -125,15 +127,16 @@ size_t rl_workspace_size(const rl_head* hd, int64_t num_rows, int32_t want_bwd) 
 }
 
 rl_status rl_batch_prepare(const rl_head* hd, const rl_batch* b, int32_t* row_seq,
-                           int32_t* active_idx, int64_t* n_active, int64_t* n_accum, void* ws,
-                           size_t ws_bytes, rl_stream_t stream) {
+                           int32_t* active_idx, int64_t* n_active, int64_t* n_accum,
+                           int64_t* nseq_accum, void* ws, size_t ws_bytes, rl_stream_t stream) {
   if (!head_ok(hd) || !batch_ok(b)) return RL_ERR_INVALID_ARG;
   WsLayout L;
   ws_layout(hd, b->num_rows, 0, &L);
   if (!ws || ws_bytes < L.total) return RL_ERR_WORKSPACE;
   if (!aligned(ws, 256)) return RL_ERR_INVALID_ARG;
   return launch_prepare(hd, b, L, static_cast<char*>(ws), row_seq, active_idx, n_active, n_accum,
-                        nullptr, nullptr, nullptr, reinterpret_cast<cudaStream_t>(stream));
+                        nseq_accum, nullptr, nullptr, nullptr,
+                        reinterpret_cast<cudaStream_t>(stream));
 }
 
 rl_status rl_logprob_fwd(const rl_head* hd, const void* hidden, const void* weight,
@@ -149,8 +152,8 @@ rl_status rl_logprob_fwd(const rl_head* hd, const void* hidden, const void* weig
   if (tc && (!aligned(hidden, 16) || !aligned(weight, 16))) return RL_ERR_INVALID_ARG;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   char* w = static_cast<char*>(ws);
-  rl_status st = launch_prepare(hd, b, L, w, nullptr, nullptr, nullptr, nullptr, logp, entropy,
-                                lse, s);
+  rl_status st = launch_prepare(hd, b, L, w, nullptr, nullptr, nullptr, nullptr, nullptr, logp,
+                                entropy, lse, s);
   if (st != RL_OK) return st;
   if (tc) {
     if ((st = launch_gather_bf16(hd, hidden, L, w, s)) != RL_OK) return st;
@@ -205,6 +208,11 @@ rl_status rl_policy_loss_fwd_bwd(const rl_head* hd, const void* hidden, const vo
   if (!(p->clip_lo >= 0.f) || !(p->clip_lo < 1.f) || !(p->clip_hi >= 0.f) ||
       !(p->logratio_clamp > 0.f) || !std::isfinite(p->loss_scale))
     return RL_ERR_INVALID_ARG;
+  if (!(p->dual_clip == 0.f || p->dual_clip > 1.f) || !(p->kl_coef >= 0.f) ||
+      !(p->entropy_coef >= 0.f) || (p->seq_mean != 0 && p->seq_mean != 1))
+    return RL_ERR_INVALID_ARG;
+  if (p->kl_coef > 0.f && b->num_rows > 0 && !p->ref_logp) return RL_ERR_INVALID_ARG;
+  const bool entropy_on = p->entropy_coef > 0.f;
   WsLayout L;
   ws_layout(hd, b->num_rows, 1, &L);
   if (!ws || ws_bytes < L.total) return RL_ERR_WORKSPACE;
@@ -215,8 +223,8 @@ rl_status rl_policy_loss_fwd_bwd(const rl_head* hd, const void* hidden, const vo
     return RL_ERR_INVALID_ARG;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   char* w = static_cast<char*>(ws);
-  rl_status st = launch_prepare(hd, b, L, w, nullptr, nullptr, nullptr, nullptr, logp, entropy,
-                                nullptr, s);
+  rl_status st = launch_prepare(hd, b, L, w, nullptr, nullptr, nullptr, nullptr, nullptr, logp,
+                                entropy, nullptr, s);
   if (st != RL_OK) return st;
   if ((st = launch_zero_inactive(hd, grad_hidden, L, w, s)) != RL_OK) return st;
   if (tc) {
@@ -242,15 +250,24 @@ rl_status rl_policy_loss_fwd_bwd(const rl_head* hd, const void* hidden, const vo
   a.clamp_c = p->logratio_clamp;
   a.loss_scale = p->loss_scale;
   a.n_global = p->n_tokens_global;
+  a.dual_clip = p->dual_clip;
+  a.kl_coef = p->kl_coef;
+  a.entropy_coef = p->entropy_coef;
+  a.seq_mean = p->seq_mean;
+  a.ref_logp = p->kl_coef > 0.f ? p->ref_logp : nullptr;
+  a.n_seqs_global = p->n_seqs_global;
+  a.cu_seqlens = b->cu_seqlens;
   a.g_c = reinterpret_cast<float*>(w + L.off_g);
   a.lse_c = reinterpret_cast<float*>(w + L.off_lse);
+  a.ge_c = entropy_on ? reinterpret_cast<float*>(w + L.off_ge) : nullptr;
+  a.ez_c = entropy_on ? reinterpret_cast<float*>(w + L.off_ez) : nullptr;
   a.st_d = reinterpret_cast<double*>(w + L.off_st_d);
   a.st_f = reinterpret_cast<float*>(w + L.off_st_f);
   a.st_i = reinterpret_cast<long long*>(w + L.off_st_i);
   if ((st = launch_merge(L, w, a, s)) != RL_OK) return st;
   if ((st = launch_stats_reduce(L, w, stats, s)) != RL_OK) return st;
-  if (tc) return launch_tc_bwd(hd, weight, grad_hidden, grad_weight, L, w, s);
-  return launch_simt_bwd(hd, hidden, weight, grad_hidden, grad_weight, L, w, s);
+  if (tc) return launch_tc_bwd(hd, weight, grad_hidden, grad_weight, entropy_on, L, w, s);
+  return launch_simt_bwd(hd, hidden, weight, grad_hidden, grad_weight, entropy_on, L, w, s);
 }
 
 const char* rl_status_string(rl_status s) {

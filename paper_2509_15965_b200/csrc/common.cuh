@@ -45,8 +45,8 @@ struct WsLayout {
   int64_t nblk_rows;      // 1024-row blocks of the bookkeeping kernels
   int64_t nblk_loss;      // 256-row blocks of the merge/loss kernel
   size_t off_hdr, off_flags, off_blkcnt, off_blkoff, off_active, off_rowseq, off_tgt,
-      off_seq, off_hc, off_pm, off_ps, off_pu, off_zy, off_lse, off_g, off_dz, off_st_d,
-      off_st_f, off_st_i, total;
+      off_seq, off_hc, off_pm, off_ps, off_pu, off_zy, off_lse, off_g, off_ge, off_ez, off_dz,
+      off_st_d, off_st_f, off_st_i, total;
 };
 bool ws_layout(const rl_head* hd, int64_t R, int want_bwd, WsLayout* L);
 

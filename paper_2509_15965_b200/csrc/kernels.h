@@ -10,8 +10,8 @@ namespace rlh {
 // given). Zeroes zero0..2 [R] (fp32, may be NULL) on inactive rows.
 rl_status launch_prepare(const rl_head* hd, const rl_batch* b, const WsLayout& L, char* ws,
                          int32_t* row_seq_user, int32_t* active_idx_user, int64_t* n_active_user,
-                         int64_t* n_accum, float* zero0, float* zero1, float* zero2,
-                         cudaStream_t s);
+                         int64_t* n_accum, int64_t* nseq_accum, float* zero0, float* zero1,
+                         float* zero2, cudaStream_t s);
 // Compact bf16 rows Hc[r] = hidden[active_idx[r]], zero rows up to the tile.
 rl_status launch_gather_bf16(const rl_head* hd, const void* hidden, const WsLayout& L, char* ws,
                              cudaStream_t s);
@@ -36,8 +36,15 @@ struct MergeArgs {
   float clip_lo, clip_hi, clamp_c;
   double loss_scale;
   const int64_t* n_global;
+  // NEXT-1 variants
+  float dual_clip, kl_coef, entropy_coef;
+  int32_t seq_mean;
+  const float* ref_logp;                // row space
+  const int64_t* n_seqs_global;
+  const int32_t* cu_seqlens;            // for n_s (seq_mean)
   float *g_c, *lse_c;                   // compact, for the backward
-  double* st_d;                         // [nblk][3] loss, ratio, entropy sums
+  float *ge_c, *ez_c;                   // compact: w c_ent and E_p[z] (entropy bonus)
+  double* st_d;                         // [nblk][5] loss, ratio, entropy, kl, objective
   float* st_f;                          // [nblk] ratio max
   long long* st_i;                      // [nblk][3] clip_lo, clip_hi, tokens
 };
@@ -48,14 +55,15 @@ rl_status launch_stats_reduce(const WsLayout& L, char* ws, rl_loss_stats* stats,
 rl_status launch_simt_fwd(const rl_head* hd, const void* hidden, const void* weight,
                           const WsLayout& L, char* ws, cudaStream_t s);
 rl_status launch_simt_bwd(const rl_head* hd, const void* hidden, const void* weight,
-                          void* grad_hidden, float* grad_weight, const WsLayout& L, char* ws,
-                          cudaStream_t s);
+                          void* grad_hidden, float* grad_weight, bool entropy_on,
+                          const WsLayout& L, char* ws, cudaStream_t s);
 
 // Tensor-core path (bf16, tcgen05/TMEM/TMA).
 rl_status launch_tc_fwd(const rl_head* hd, const void* weight, const WsLayout& L, char* ws,
                         cudaStream_t s);
 rl_status launch_tc_bwd(const rl_head* hd, const void* weight, void* grad_hidden,
-                        float* grad_weight, const WsLayout& L, char* ws, cudaStream_t s);
+                        float* grad_weight, bool entropy_on, const WsLayout& L, char* ws,
+                        cudaStream_t s);
 
 int num_sms();
 

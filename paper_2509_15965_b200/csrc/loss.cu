@@ -4,7 +4,9 @@
 //    (entropy in the shifted form avoids cancelling M), logp = z_y - lse;
 //  * H5 (P:L828 token-level mean, readings DESIGN.md §3 #12-#15):
 //    d = logp - old, r = exp(clamp(d)), l = max(-A r, -A clip(r)),
-//    g = dL/dlogp = -scale * A r [unclipped] [|d| <= c];
+//    g = dL/dlogp = -w A r [unclipped] [|d| <= c]; NEXT-1 variants (#25-#28):
+//    dual clip, KL-k3 to ref_logp, entropy bonus (w c_ent and E_p[z] kept for
+//    the dZ epilogue), seq-mean-token-mean weights w = 1/(S n_s);
 //  * per-block fixed-order reduction of the loss statistics (deterministic),
 //    summed by a one-block kernel into the caller's accumulators.
 #include "kernels.h"
@@ -14,7 +16,7 @@ namespace rlh {
 constexpr int MERGE_THREADS = 256;
 
 struct LStat {
-  double loss, ratio, ent;
+  double loss, ratio, ent, kl, obj;
   float rmax;
   long long clo, chi, tok;
 };
@@ -23,6 +25,8 @@ __device__ __forceinline__ void lstat_add(LStat& a, const LStat& b) {
   a.loss += b.loss;
   a.ratio += b.ratio;
   a.ent += b.ent;
+  a.kl += b.kl;
+  a.obj += b.obj;
   a.rmax = fmaxf(a.rmax, b.rmax);
   a.clo += b.clo;
   a.chi += b.chi;
@@ -34,6 +38,8 @@ __device__ __forceinline__ LStat lstat_shfl(const LStat& v, int o) {
   w.loss = __shfl_xor_sync(0xffffffffu, v.loss, o);
   w.ratio = __shfl_xor_sync(0xffffffffu, v.ratio, o);
   w.ent = __shfl_xor_sync(0xffffffffu, v.ent, o);
+  w.kl = __shfl_xor_sync(0xffffffffu, v.kl, o);
+  w.obj = __shfl_xor_sync(0xffffffffu, v.obj, o);
   w.rmax = __shfl_xor_sync(0xffffffffu, v.rmax, o);
   w.clo = __shfl_xor_sync(0xffffffffu, v.clo, o);
   w.chi = __shfl_xor_sync(0xffffffffu, v.chi, o);
@@ -56,12 +62,23 @@ __device__ LStat block_reduce_lstat(LStat v) {
   return t;
 }
 
+// First index i in [0, T) with active_idx[i] >= row (active_idx ascending).
+__device__ __forceinline__ int64_t lower_bound_rows(const int32_t* __restrict__ a, int64_t T,
+                                                   int64_t row) {
+  int64_t lo = 0, hi = T;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (static_cast<int64_t>(a[mid]) < row) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
 template <bool LOSS>
 __global__ void __launch_bounds__(MERGE_THREADS)
 k_merge(MergeArgs a, const WsHeader* __restrict__ hdr, int64_t n_vt, int64_t ldp) {
   const int64_t T = hdr->n_active;
   const int64_t r = static_cast<int64_t>(blockIdx.x) * MERGE_THREADS + threadIdx.x;
-  LStat st{0.0, 0.0, 0.0, 0.f, 0, 0, 0};
+  LStat st{0.0, 0.0, 0.0, 0.0, 0.0, 0.f, 0, 0, 0};
   if (r < T) {
     float M = a.pm[r], S = a.ps[r], U = a.pu[r];
     for (int64_t n = 1; n < n_vt; ++n) {
@@ -85,39 +102,74 @@ k_merge(MergeArgs a, const WsHeader* __restrict__ hdr, int64_t n_vt, int64_t ldp
     if (a.entropy) a.entropy[t] = ent;
     if (a.lse) a.lse[t] = lse;
     if constexpr (LOSS) {
-      double scale = a.loss_scale;
-      if (a.n_global) {
+      const int32_t sq = a.seq_c[r];
+      // per-token weight w_t (token mean: 1/N; seq-mean-token-mean: 1/(S n_s))
+      double base = a.loss_scale;
+      if (a.seq_mean) {
+        if (a.n_seqs_global) {
+          const long long Sg = *a.n_seqs_global;
+          base = Sg > 0 ? 1.0 / static_cast<double>(Sg) : 0.0;
+        }
+        // active rows of sequence sq are the compact range [lb(cu[sq]), lb(cu[sq+1]))
+        const int64_t b0 = lower_bound_rows(a.active_idx, T, a.cu_seqlens[sq]);
+        const int64_t b1 = lower_bound_rows(a.active_idx, T, a.cu_seqlens[sq + 1]);
+        base /= static_cast<double>(b1 - b0);
+      } else if (a.n_global) {
         const long long N = *a.n_global;
-        scale = N > 0 ? 1.0 / static_cast<double>(N) : 0.0;
+        base = N > 0 ? 1.0 / static_cast<double>(N) : 0.0;
       }
-      const float A = a.adv[a.seq_c[r]];
+      const float A = a.adv[sq];
       const float d = lp - a.old_logp[t];
       const float dc = fminf(fmaxf(d, -a.clamp_c), a.clamp_c);
       const float ratio = expf(dc);
       const float lo = 1.f - a.clip_lo, hi = 1.f + a.clip_hi;
       const float rc = fminf(fmaxf(ratio, lo), hi);
-      const float loss = fmaxf(-A * ratio, -A * rc);
+      float loss = fmaxf(-A * ratio, -A * rc);
       const bool chi = (A > 0.f) && (ratio > hi);
       const bool clo = (A < 0.f) && (ratio < lo);
-      const bool flows = !(chi || clo) && (fabsf(d) <= a.clamp_c);
-      const float g = flows ? static_cast<float>(-scale * static_cast<double>(A) * ratio) : 0.f;
-      a.g_c[r] = g;
+      bool flows = !(chi || clo) && (fabsf(d) <= a.clamp_c);
+      if (a.dual_clip > 0.f && A < 0.f) {  // dual clip: cap the loss at -A c_dual
+        loss = fminf(loss, -A * a.dual_clip);
+        if (ratio > a.dual_clip) flows = false;
+      }
+      double dl = flows ? -static_cast<double>(A) * ratio : 0.0;
+      float kl = 0.f;
+      if (a.ref_logp) {  // k3 estimator of KL to the reference policy
+        const float q0 = a.ref_logp[t] - lp;
+        const float q = fminf(fmaxf(q0, -a.clamp_c), a.clamp_c);
+        const float eq = expf(q);
+        kl = eq - q - 1.f;
+        if (fabsf(q0) <= a.clamp_c) dl += static_cast<double>(a.kl_coef) * (1.0 - eq);
+      }
+      a.g_c[r] = static_cast<float>(base * dl);
       a.lse_c[r] = lse;
+      if (a.ge_c) {
+        a.ge_c[r] = static_cast<float>(base * a.entropy_coef);
+        a.ez_c[r] = lse - ent;  // E_p[z]
+      }
+      const double obj = base * (static_cast<double>(loss) + a.kl_coef * static_cast<double>(kl) -
+                                 a.entropy_coef * static_cast<double>(ent));
       st = {static_cast<double>(loss), static_cast<double>(ratio), static_cast<double>(ent),
-            ratio, clo ? 1ll : 0ll, chi ? 1ll : 0ll, 1ll};
+            static_cast<double>(kl), obj, ratio, clo ? 1ll : 0ll, chi ? 1ll : 0ll, 1ll};
     }
   } else if (r < ldp) {
-    if constexpr (LOSS) {  // padding rows of the last tile: zero gradient coefficient
+    if constexpr (LOSS) {  // padding rows of the last tile: zero gradient coefficients
       a.g_c[r] = 0.f;
       a.lse_c[r] = 0.f;
+      if (a.ge_c) {
+        a.ge_c[r] = 0.f;
+        a.ez_c[r] = 0.f;
+      }
     }
   }
   if constexpr (LOSS) {
     st = block_reduce_lstat<MERGE_THREADS>(st);
     if (threadIdx.x == 0) {
-      a.st_d[3 * blockIdx.x] = st.loss;
-      a.st_d[3 * blockIdx.x + 1] = st.ratio;
-      a.st_d[3 * blockIdx.x + 2] = st.ent;
+      a.st_d[5 * blockIdx.x] = st.loss;
+      a.st_d[5 * blockIdx.x + 1] = st.ratio;
+      a.st_d[5 * blockIdx.x + 2] = st.ent;
+      a.st_d[5 * blockIdx.x + 3] = st.kl;
+      a.st_d[5 * blockIdx.x + 4] = st.obj;
       a.st_f[blockIdx.x] = st.rmax;
       a.st_i[3 * blockIdx.x] = st.clo;
       a.st_i[3 * blockIdx.x + 1] = st.chi;
@@ -143,9 +195,10 @@ rl_status launch_merge(const WsLayout& L, char* ws, const MergeArgs& a, cudaStre
 __global__ void __launch_bounds__(MERGE_THREADS)
 k_stats_reduce(const double* __restrict__ st_d, const float* __restrict__ st_f,
                const long long* __restrict__ st_i, int64_t nblk, rl_loss_stats* out) {
-  LStat v{0.0, 0.0, 0.0, 0.f, 0, 0, 0};
+  LStat v{0.0, 0.0, 0.0, 0.0, 0.0, 0.f, 0, 0, 0};
   for (int64_t b = threadIdx.x; b < nblk; b += MERGE_THREADS) {
-    LStat w{st_d[3 * b], st_d[3 * b + 1], st_d[3 * b + 2], st_f[b], st_i[3 * b], st_i[3 * b + 1],
+    LStat w{st_d[5 * b],     st_d[5 * b + 1], st_d[5 * b + 2], st_d[5 * b + 3],
+            st_d[5 * b + 4], st_f[b],         st_i[3 * b],     st_i[3 * b + 1],
             st_i[3 * b + 2]};
     lstat_add(v, w);
   }
@@ -154,6 +207,8 @@ k_stats_reduce(const double* __restrict__ st_d, const float* __restrict__ st_f,
     out->loss_sum += v.loss;
     out->ratio_sum += v.ratio;
     out->entropy_sum += v.ent;
+    out->kl_sum += v.kl;
+    out->objective += v.obj;
     out->ratio_max = fmaxf(out->ratio_max, v.rmax);
     out->clip_lo_count += v.clo;
     out->clip_hi_count += v.chi;

@@ -143,10 +143,35 @@ k_compact(int64_t R, const uint8_t* __restrict__ act, const int32_t* __restrict_
   }
 }
 
+// First index i in [0, T) with active_idx[i] >= row (active_idx ascending).
+__device__ __forceinline__ int64_t lower_bound_rows(const int32_t* __restrict__ a, int64_t T,
+                                                   int64_t row) {
+  int64_t lo = 0, hi = T;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (static_cast<int64_t>(a[mid]) < row) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// Sequences with at least one active row (the seq-mean normaliser S).
+__global__ void __launch_bounds__(PREP_THREADS)
+k_seq_count(const int32_t* __restrict__ cu, int32_t S, const int32_t* __restrict__ active_idx,
+            const WsHeader* __restrict__ hdr, int64_t* nseq_accum) {
+  const int64_t T = hdr->n_active;
+  const int s = blockIdx.x * PREP_THREADS + threadIdx.x;
+  int nonempty = 0;
+  if (s < S && !hdr->bad_cu)
+    nonempty = lower_bound_rows(active_idx, T, cu[s + 1]) > lower_bound_rows(active_idx, T, cu[s]);
+  const int c = __syncthreads_count(nonempty);
+  if (threadIdx.x == 0 && c)
+    atomicAdd(reinterpret_cast<unsigned long long*>(nseq_accum), static_cast<unsigned long long>(c));
+}
+
 rl_status launch_prepare(const rl_head* hd, const rl_batch* b, const WsLayout& L, char* ws,
                          int32_t* row_seq_user, int32_t* active_idx_user, int64_t* n_active_user,
-                         int64_t* n_accum, float* zero0, float* zero1, float* zero2,
-                         cudaStream_t s) {
+                         int64_t* n_accum, int64_t* nseq_accum, float* zero0, float* zero1,
+                         float* zero2, cudaStream_t s) {
   WsHeader* hdr = reinterpret_cast<WsHeader*>(ws + L.off_hdr);
   uint8_t* act = reinterpret_cast<uint8_t*>(ws + L.off_flags);
   int32_t* blk_cnt = reinterpret_cast<int32_t*>(ws + L.off_blkcnt);
@@ -180,6 +205,12 @@ rl_status launch_prepare(const rl_head* hd, const rl_batch* b, const WsLayout& L
     k_compact<<<static_cast<unsigned>(nblk), PREP_THREADS, 0, s>>>(R, act, row_seq, b->targets,
                                                                     blk_off, active_idx, tgt_c,
                                                                     seq_c);
+  }
+  RLH_CHECK_LAUNCH();
+  if (nseq_accum && b->num_seqs > 0) {
+    TraceScope ts(RL_K_PREPARE, s);
+    k_seq_count<<<static_cast<unsigned>(ceil_div(b->num_seqs, PREP_THREADS)), PREP_THREADS, 0,
+                  s>>>(b->cu_seqlens, b->num_seqs, active_idx, hdr, nseq_accum);
   }
   RLH_CHECK_LAUNCH();
   return RL_OK;

@@ -84,6 +84,7 @@ k_simt_dz(const T* __restrict__ hidden, int64_t ld, const T* __restrict__ W, int
           float inv_temp, const int32_t* __restrict__ active_idx,
           const int32_t* __restrict__ tgt_c, const WsHeader* __restrict__ hdr,
           const float* __restrict__ lse_c, const float* __restrict__ g_c,
+          const float* __restrict__ ge_c, const float* __restrict__ ez_c,
           float* __restrict__ dz) {
   extern __shared__ float hs[];
   const int64_t T_ = hdr->n_active;
@@ -93,10 +94,12 @@ k_simt_dz(const T* __restrict__ hidden, int64_t ld, const T* __restrict__ W, int
     __syncthreads();
     const int y = tgt_c[r];
     const float lse = lse_c[r], coef = g_c[r] * inv_temp;
+    const float cent = ge_c ? ge_c[r] * inv_temp : 0.f, ez = ge_c ? ez_c[r] : 0.f;
     for (int v = threadIdx.x; v < V; v += SIMT_THREADS) {
       const float z = simt_logit(hs, W + static_cast<int64_t>(v) * h, h, inv_temp);
       const float p = expf(z - lse);
-      dz[r * V + v] = coef * ((v == y ? 1.f : 0.f) - p);
+      // g (onehot - p) + w c_ent p (z - E_p z)  (entropy bonus; 0 when off)
+      dz[r * V + v] = coef * ((v == y ? 1.f : 0.f) - p) + cent * p * (z - ez);
     }
     __syncthreads();
   }
@@ -199,8 +202,8 @@ static rl_status simt_fwd_t(const rl_head* hd, const void* hidden, const void* w
 
 template <typename T>
 static rl_status simt_bwd_t(const rl_head* hd, const void* hidden, const void* weight,
-                            void* grad_hidden, float* grad_weight, const WsLayout& L, char* ws,
-                            cudaStream_t s) {
+                            void* grad_hidden, float* grad_weight, bool entropy_on,
+                            const WsLayout& L, char* ws, cudaStream_t s) {
   const WsHeader* hdr = reinterpret_cast<const WsHeader*>(ws + L.off_hdr);
   const int32_t* active_idx = reinterpret_cast<const int32_t*>(ws + L.off_active);
   float* dz = reinterpret_cast<float*>(ws + L.off_dz);
@@ -218,7 +221,8 @@ static rl_status simt_bwd_t(const rl_head* hd, const void* hidden, const void* w
         static_cast<const T*>(hidden), hd->ld_hidden, static_cast<const T*>(weight), h, V,
         hd->inv_temperature, active_idx, reinterpret_cast<const int32_t*>(ws + L.off_tgt), hdr,
         reinterpret_cast<const float*>(ws + L.off_lse), reinterpret_cast<const float*>(ws + L.off_g),
-        dz);
+        entropy_on ? reinterpret_cast<const float*>(ws + L.off_ge) : nullptr,
+        entropy_on ? reinterpret_cast<const float*>(ws + L.off_ez) : nullptr, dz);
   }
   RLH_CHECK_LAUNCH();
   {
@@ -250,11 +254,13 @@ rl_status launch_simt_fwd(const rl_head* hd, const void* hidden, const void* wei
                              : simt_fwd_t<__nv_bfloat16>(hd, hidden, weight, L, ws, s);
 }
 rl_status launch_simt_bwd(const rl_head* hd, const void* hidden, const void* weight,
-                          void* grad_hidden, float* grad_weight, const WsLayout& L, char* ws,
-                          cudaStream_t s) {
+                          void* grad_hidden, float* grad_weight, bool entropy_on,
+                          const WsLayout& L, char* ws, cudaStream_t s) {
   return hd->dtype == RL_F32
-             ? simt_bwd_t<float>(hd, hidden, weight, grad_hidden, grad_weight, L, ws, s)
-             : simt_bwd_t<__nv_bfloat16>(hd, hidden, weight, grad_hidden, grad_weight, L, ws, s);
+             ? simt_bwd_t<float>(hd, hidden, weight, grad_hidden, grad_weight, entropy_on, L, ws,
+                                 s)
+             : simt_bwd_t<__nv_bfloat16>(hd, hidden, weight, grad_hidden, grad_weight, entropy_on,
+                                         L, ws, s);
 }
 
 }  // namespace rlh

@@ -79,6 +79,7 @@ struct TcArgs {
   int64_t ldp;
   // EPI_DZ
   const float *lse_c, *g_c;
+  const float *ge_c, *ez_c;  // entropy bonus (NULL = off): w c_ent and E_p[z]
   __nv_bfloat16* dz;
   int64_t ld_dz;
   // EPI_ROWS
@@ -341,6 +342,10 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         const float lse2 = lse * LOG2E, sc2 = args.inv_temp * LOG2E;
         uint4* dst = reinterpret_cast<uint4*>(args.dz + row * args.ld_dz + n0);
         const uint64_t st_pol = l2_policy_evict_first();  // 17 GB stream: keep W/Hc in L2
+        // entropy bonus: + tau^-1 w c_ent p (z - E_p z); off -> cent = 0 (warp-uniform)
+        const bool ent_on = args.ge_c != nullptr;
+        const float cent = (ent_on && row_ok) ? args.ge_c[row] * args.inv_temp : 0.f;
+        const float ez = (ent_on && row_ok) ? args.ez_c[row] : 0.f;
 #pragma unroll 1
         for (int c = 0; c < TC_BN / 32; ++c) {
           uint32_t v[32];
@@ -348,13 +353,27 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           tmem_ld_wait();
           if (c == TC_BN / 32 - 1) release(acc);
           uint32_t pk[16];
+          if (!ent_on) {
 #pragma unroll
-          for (int j = 0; j < 32; j += 2) {
-            const float p0 = ex2_approx(fmaf(__uint_as_float(v[j]), sc2, -lse2));
-            const float p1 = ex2_approx(fmaf(__uint_as_float(v[j + 1]), sc2, -lse2));
-            const float d0 = coef * ((c * 32 + j == yrel ? 1.f : 0.f) - p0);
-            const float d1 = coef * ((c * 32 + j + 1 == yrel ? 1.f : 0.f) - p1);
-            pk[j / 2] = pack_bf16x2(d0, d1);
+            for (int j = 0; j < 32; j += 2) {
+              const float p0 = ex2_approx(fmaf(__uint_as_float(v[j]), sc2, -lse2));
+              const float p1 = ex2_approx(fmaf(__uint_as_float(v[j + 1]), sc2, -lse2));
+              const float d0 = coef * ((c * 32 + j == yrel ? 1.f : 0.f) - p0);
+              const float d1 = coef * ((c * 32 + j + 1 == yrel ? 1.f : 0.f) - p1);
+              pk[j / 2] = pack_bf16x2(d0, d1);
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; j += 2) {
+              const float z0 = __uint_as_float(v[j]) * args.inv_temp;
+              const float z1 = __uint_as_float(v[j + 1]) * args.inv_temp;
+              const float p0 = ex2_approx(fmaf(__uint_as_float(v[j]), sc2, -lse2));
+              const float p1 = ex2_approx(fmaf(__uint_as_float(v[j + 1]), sc2, -lse2));
+              const float d0 = coef * ((c * 32 + j == yrel ? 1.f : 0.f) - p0) + cent * p0 * (z0 - ez);
+              const float d1 =
+                  coef * ((c * 32 + j + 1 == yrel ? 1.f : 0.f) - p1) + cent * p1 * (z1 - ez);
+              pk[j / 2] = pack_bf16x2(d0, d1);
+            }
           }
 #pragma unroll
           for (int q = 0; q < 4; ++q)
@@ -579,7 +598,8 @@ rl_status launch_tc_fwd(const rl_head* hd, const void* weight, const WsLayout& L
 }
 
 rl_status launch_tc_bwd(const rl_head* hd, const void* weight, void* grad_hidden,
-                        float* grad_weight, const WsLayout& L, char* ws, cudaStream_t s) {
+                        float* grad_weight, bool entropy_on, const WsLayout& L, char* ws,
+                        cudaStream_t s) {
   const int h = hd->hidden, V = hd->vocab;
   const int cg = tc_cta_group();
   __nv_bfloat16* dz = reinterpret_cast<__nv_bfloat16*>(ws + L.off_dz);
@@ -597,6 +617,10 @@ rl_status launch_tc_bwd(const rl_head* hd, const void* weight, void* grad_hidden
     t.N = V;
     t.lse_c = reinterpret_cast<const float*>(ws + L.off_lse);
     t.g_c = reinterpret_cast<const float*>(ws + L.off_g);
+    if (entropy_on) {
+      t.ge_c = reinterpret_cast<const float*>(ws + L.off_ge);
+      t.ez_c = reinterpret_cast<const float*>(ws + L.off_ez);
+    }
     t.dz = dz;
     t.ld_dz = L.Vp;
     st = run_narrow<0, 0, EPI_DZ>(ma, mb, t, L.Rp, RL_K_GEMM_DZ, s);

@@ -82,12 +82,12 @@ def all_reduce_(t, op="sum", group=None):
 
 
 def reduce_stats_(stats_u8, group=None):
-    """All-reduce a device rl_loss_stats (56 bytes): sums for the fp64/int64
+    """All-reduce a device rl_loss_stats (72 bytes): sums for the fp64/int64
     fields, max for ratio_max."""
     import torch
-    d = stats_u8[:24].view(torch.float64)
-    f = stats_u8[24:28].view(torch.float32)
-    i = stats_u8[32:56].view(torch.int64)
+    d = stats_u8[:40].view(torch.float64)
+    f = stats_u8[40:44].view(torch.float32)
+    i = stats_u8[48:72].view(torch.int64)
     all_reduce_(d, "sum", group)
     all_reduce_(f, "max", group)
     all_reduce_(i, "sum", group)
@@ -142,7 +142,9 @@ class PolicyLossStep:
         self.group = group
         dev = weight.device
         self.n_global = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.n_seqs = torch.zeros(1, dtype=torch.int64, device=dev)
         self.params.n_tokens_global = self.n_global
+        self.params.n_seqs_global = self.n_seqs
         self.adv = torch.empty(max(db.cu.shape[0] - 1, 1), dtype=torch.float32, device=dev)
         self.grad_w = torch.zeros(weight.shape[0], weight.shape[1], dtype=torch.float32, device=dev)
         self.stats = R.new_stats(dev)
@@ -151,12 +153,15 @@ class PolicyLossStep:
         self.ws_prep = R.Workspace(dev)
 
     def count_tokens(self):
-        """N = masked tokens of the whole mini-batch over all ranks."""
+        """N = masked tokens (and S = non-empty sequences, for seq-mean
+        aggregation) of the whole mini-batch over all ranks."""
         R = self.R
         self.n_global.zero_()
+        self.n_seqs.zero_()
         R.rl_batch_prepare(self.head, R.Batch(self.db.cu, self.db.targets, self.db.mask),
-                           n_accum=self.n_global, ws=self.ws_prep)
+                           n_accum=self.n_global, nseq_accum=self.n_seqs, ws=self.ws_prep)
         all_reduce_(self.n_global, "sum", self.group)
+        all_reduce_(self.n_seqs, "sum", self.group)
 
     def advantages(self):
         self.R.rl_grpo_advantage(self.db.rewards, self.db.gos, self.db.num_groups, self.adv)

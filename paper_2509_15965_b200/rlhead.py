@@ -39,12 +39,14 @@ class rl_head(C.Structure):
 
 class rl_loss_params(C.Structure):
     _fields_ = [("clip_lo", C.c_float), ("clip_hi", C.c_float), ("logratio_clamp", C.c_float),
-                ("loss_scale", C.c_double), ("n_tokens_global", C.c_void_p)]
+                ("loss_scale", C.c_double), ("n_tokens_global", C.c_void_p),
+                ("dual_clip", C.c_float), ("kl_coef", C.c_float), ("entropy_coef", C.c_float),
+                ("seq_mean", C.c_int32), ("ref_logp", C.c_void_p), ("n_seqs_global", C.c_void_p)]
 
 
 class rl_loss_stats(C.Structure):
     _fields_ = [("loss_sum", C.c_double), ("ratio_sum", C.c_double), ("entropy_sum", C.c_double),
-                ("ratio_max", C.c_float), ("reserved", C.c_int32), ("clip_lo_count", C.c_int64),
+                ("kl_sum", C.c_double), ("objective", C.c_double), ("ratio_max", C.c_float), ("reserved", C.c_int32), ("clip_lo_count", C.c_int64),
                 ("clip_hi_count", C.c_int64), ("tokens", C.c_int64)]
 
 
@@ -55,7 +57,7 @@ lib.rl_workspace_size.restype = C.c_size_t
 lib.rl_workspace_size.argtypes = [C.POINTER(rl_head), C.c_int64, C.c_int32]
 lib.rl_batch_prepare.restype = C.c_int
 lib.rl_batch_prepare.argtypes = [C.POINTER(rl_head), C.POINTER(rl_batch), _vp, _vp, _vp, _vp,
-                                 _vp, _sz, _vp]
+                                 _vp, _vp, _sz, _vp]
 lib.rl_logprob_fwd.restype = C.c_int
 lib.rl_logprob_fwd.argtypes = [C.POINTER(rl_head), _vp, _vp, C.POINTER(rl_batch), _vp, _vp, _vp,
                                _vp, _sz, _vp]
@@ -138,15 +140,24 @@ class Batch:
 
 @dataclass
 class LossParams:
+    """rl_loss_params (include/rlhead.h); defaults = GRPO/DAPO token-mean loss."""
     clip_lo: float = 0.2
     clip_hi: float = 0.2
     logratio_clamp: float = 20.0
     loss_scale: float = 1.0
     n_tokens_global: object = None  # device int64[1] tensor: scale = 1/N
+    dual_clip: float = 0.0
+    kl_coef: float = 0.0
+    entropy_coef: float = 0.0
+    seq_mean: bool = False
+    ref_logp: object = None         # device fp32 [R] (needed when kl_coef > 0)
+    n_seqs_global: object = None    # device int64[1]: S for seq_mean
 
     def c(self) -> rl_loss_params:
         return rl_loss_params(self.clip_lo, self.clip_hi, self.logratio_clamp, self.loss_scale,
-                              _ptr(self.n_tokens_global))
+                              _ptr(self.n_tokens_global), self.dual_clip, self.kl_coef,
+                              self.entropy_coef, int(bool(self.seq_mean)), _ptr(self.ref_logp),
+                              _ptr(self.n_seqs_global))
 
 
 class Workspace:
@@ -185,14 +196,14 @@ def rl_workspace_size(head: Head, num_rows: int, want_bwd: bool) -> int:
 
 
 def rl_batch_prepare(head: Head, batch: Batch, row_seq=None, active_idx=None, n_active=None,
-                     n_accum=None, ws: Workspace | None = None, stream=None):
+                     n_accum=None, nseq_accum=None, ws: Workspace | None = None, stream=None):
     hd, b = head.c(), batch.c()
     ws = ws or Workspace()
     nb = rl_workspace_size(head, b.num_rows, False)
     buf = ws.get(nb)
     _check(lib.rl_batch_prepare(C.byref(hd), C.byref(b), _ptr(row_seq), _ptr(active_idx),
-                                _ptr(n_active), _ptr(n_accum), _ptr(buf), buf.numel(),
-                                _stream(stream)), "rl_batch_prepare")
+                                _ptr(n_active), _ptr(n_accum), _ptr(nseq_accum), _ptr(buf),
+                                buf.numel(), _stream(stream)), "rl_batch_prepare")
 
 
 def rl_logprob_fwd(head: Head, hidden, weight, batch: Batch, logp, entropy=None, lse=None,

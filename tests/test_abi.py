@@ -43,7 +43,8 @@ def test_workspace_size_and_validation_host_only():
     st = R.lib.rl_logprob_fwd(None, None, None, None, None, None, None, None, 0, None)
     assert st == R.RL_ERR_INVALID_ARG
     b = R.rl_batch(4, 1, None, None, None, None)
-    st = R.lib.rl_batch_prepare(C.byref(hd), C.byref(b), None, None, None, None, None, 0, None)
+    st = R.lib.rl_batch_prepare(C.byref(hd), C.byref(b), None, None, None, None, None, None, 0,
+                                None)
     assert st == R.RL_ERR_INVALID_ARG
     assert R.lib.rl_status_string(3) == b"RL_ERR_WORKSPACE"
     assert R.lib.rl_grpo_advantage(None, None, -1, 1, None, None, 1e-6, 1, None, None, None) \

@@ -60,8 +60,9 @@ def _free_port():
 
 def _stats_bytes(d):
     from paper_2509_15965_b200 import rlhead as R
-    s = R.rl_loss_stats(d["loss_sum"], d["ratio_sum"], d["entropy_sum"], d["ratio_max"], 0,
-                        d["clip_lo_count"], d["clip_hi_count"], d["tokens"])
+    s = R.rl_loss_stats(d["loss_sum"], d["ratio_sum"], d["entropy_sum"], d["kl_sum"],
+                        d["objective"], d["ratio_max"], 0, d["clip_lo_count"],
+                        d["clip_hi_count"], d["tokens"])
     return bytes(s)
 
 

@@ -76,13 +76,19 @@ typedef struct {
  * `dtype`; weight is W[vocab, hidden] row-major (nn.Linear layout), same
  * dtype, densely packed (row stride = hidden). logits = inv_temperature*H W^T.
  * RL_BF16 runs the tcgen05/TMEM/TMA tensor-core path and needs hidden % 64
- * == 0 and ld_hidden % 8 == 0; RL_F32 runs the exact-fp32 CUDA-core path. */
+ * == 0 and ld_hidden % 8 == 0; RL_F32 runs the exact-fp32 CUDA-core path.
+ * Vocab-parallel head (NEXT-3, tensor parallelism as the paper's actor TP,
+ * P:L783): `weight` holds rows [vocab_offset, vocab_offset + vocab) of a
+ * vocab_total-row head; targets stay GLOBAL ids in [0, vocab_total).
+ * vocab_total = 0 means unsharded (vocab_total = vocab, offset 0). */
 typedef struct {
   int32_t hidden;        /* h  (1..65536)                                      */
-  int32_t vocab;         /* V  (1..2^24)                                       */
+  int32_t vocab;         /* V  (1..2^24): rows of `weight` on this rank         */
   rl_dtype dtype;        /* RL_F32 | RL_BF16                                   */
   int64_t ld_hidden;     /* row stride of hidden / grad_hidden in elements >= h */
   float inv_temperature; /* tau^-1 > 0 (1 = plain softmax)                     */
+  int64_t vocab_offset;  /* first global vocab id held by `weight` (sharded)   */
+  int64_t vocab_total;   /* full vocabulary (0 = unsharded)                    */
 } rl_head;
 
 /* Workspace bytes for a call on up to `num_rows` packed rows;
@@ -192,6 +198,34 @@ RL_API rl_status rl_policy_loss_fwd_bwd(const rl_head *hd, const void *hidden, c
                                  const rl_loss_params *p, float *logp, float *entropy,
                                  void *grad_hidden, float *grad_weight, rl_loss_stats *stats,
                                  void *ws, size_t ws_bytes, rl_stream_t stream);
+
+/* ---- vocab-parallel head (NEXT-3) ----------------------
+ * A vocab shard cannot finish the log-sum-exp alone. Phase 1 on every rank:
+ *   rl_logprob_partials -> parts [4][num_rows] fp32 for THIS shard, in compact
+ *   (active-row) order: (m, s = sum e^{z-m}, u = sum e^{z-m}(z-m), z_y or 0
+ *   when the target is not in this shard); entries >= n_active unspecified.
+ * The caller all-gathers parts over the TP group -> parts_all [P][4][num_rows]
+ * (P shards, any order). Phase 2, on every rank:
+ *   rl_logprob_merge            -> logp / entropy / lse (full vocabulary), or
+ *   rl_policy_loss_fwd_bwd_vp   -> as rl_policy_loss_fwd_bwd, with the softmax
+ *     over all shards; grad_hidden is this shard's PARTIAL dL/dH (the caller
+ *     all-reduces SUM over the TP group), grad_weight this shard's rows of
+ *     dL/dW (accumulated). logp/entropy/stats are identical on every rank of
+ *     the TP group (do not sum stats over TP ranks). */
+RL_API rl_status rl_logprob_partials(const rl_head *hd, const void *hidden, const void *weight,
+                                     const rl_batch *b, float *parts, void *ws, size_t ws_bytes,
+                                     rl_stream_t stream);
+RL_API rl_status rl_logprob_merge(const rl_head *hd, const rl_batch *b, const float *parts_all,
+                                  int32_t nparts, float *logp, float *entropy, float *lse,
+                                  void *ws, size_t ws_bytes, rl_stream_t stream);
+RL_API rl_status rl_policy_loss_fwd_bwd_vp(const rl_head *hd, const void *hidden,
+                                           const void *weight, const rl_batch *b,
+                                           const float *parts_all, int32_t nparts,
+                                           const float *old_logp, const float *adv,
+                                           const rl_loss_params *p, float *logp, float *entropy,
+                                           void *grad_hidden, float *grad_weight,
+                                           rl_loss_stats *stats, void *ws, size_t ws_bytes,
+                                           rl_stream_t stream);
 
 /* ---- introspection / tracing (P:L682-690 worker timers, device-side) ---- */
 RL_API const char *rl_status_string(rl_status s);

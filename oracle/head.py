@@ -387,3 +387,47 @@ def policy_loss_fwd_bwd(hidden, weight, cu_seqlens, mask, targets, old_logp, adv
                 dH=dH, dW=dW, stats=stats, err=bk["err"], active=bk["active"],
                 row_seq=bk["row_seq"], n_active=bk["n_active"],
                 n_seqs=int((S_count > 0).sum()))
+
+
+# --------------------------------------------------------------------------
+# NEXT-3: vocab-parallel head (tensor parallelism over the vocabulary, as
+# the paper's actor TP 2/4/8). A rank holding vocab rows
+# [off, off + V_p) reports per active row (compact order) the partial
+#   m_p = max_{j in shard} z_j, s_p = sum e^{z_j - m_p},
+#   u_p = sum e^{z_j - m_p} (z_j - m_p), zy_p = z_y if y in shard else 0;
+# the log-softmax over the union of shards is then
+#   lse = log sum_p e^{m_p} s_p,  E_p[z] = sum_p e^{m_p}(u_p + m_p s_p) / sum_p e^{m_p} s_p,
+#   entropy = lse - E_p[z],  logp = sum_p zy_p - lse.
+# --------------------------------------------------------------------------
+def logprob_shard_partials(hidden, weight_shard, vocab_offset, vocab_total, cu_seqlens, mask,
+                           targets, inv_temperature=1.0):
+    """float64 [4, T] partials of one vocab shard for the active rows."""
+    Ws = _as64(weight_shard)
+    bk = bookkeeping(cu_seqlens, mask, targets, vocab_total)
+    idx = bk["active_idx"].astype(np.int64)
+    targets = np.asarray(targets).reshape(-1).astype(np.int64)
+    out = np.zeros((4, len(idx)))
+    for c0 in range(0, len(idx), _CHUNK):
+        rows = idx[c0:c0 + _CHUNK]
+        Z = (_as64(_take_rows(hidden, rows)) @ Ws.T) * inv_temperature
+        m = Z.max(axis=1)
+        E = np.exp(Z - m[:, None])
+        out[0, c0:c0 + len(rows)] = m
+        out[1, c0:c0 + len(rows)] = E.sum(axis=1)
+        out[2, c0:c0 + len(rows)] = (E * (Z - m[:, None])).sum(axis=1)
+        yl = targets[rows] - vocab_offset
+        own = (yl >= 0) & (yl < Ws.shape[0])
+        out[3, c0:c0 + len(rows)] = np.where(own, Z[np.arange(len(rows)), np.clip(yl, 0, Ws.shape[0] - 1)], 0.0)
+    return out
+
+
+def merge_shard_partials(parts):
+    """parts [P, 4, T] -> dict(lse, entropy, logp) per compact row (float64)."""
+    parts = np.asarray(parts, dtype=np.float64)
+    m, s, u, zy = parts[:, 0], parts[:, 1], parts[:, 2], parts[:, 3]
+    M = m.max(axis=0)                          # shift for range only
+    w = np.exp(m - M) * s                      # e^{m_p - M} s_p
+    S = w.sum(axis=0)
+    lse = M + np.log(S)
+    Ez = (np.exp(m - M) * (u + m * s)).sum(axis=0) / S
+    return dict(lse=lse, entropy=lse - Ez, logp=zy.sum(axis=0) - lse)

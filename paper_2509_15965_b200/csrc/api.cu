@@ -98,6 +98,11 @@ static bool head_ok(const rl_head* hd) {
   if (!(hd->inv_temperature > 0.f) || !std::isfinite(hd->inv_temperature)) return false;
   if (hd->dtype == RL_F32 && hd->hidden > 12288) return false;  // SIMT smem row cache
   if (use_tc(hd) && (hd->hidden % 64 != 0 || hd->ld_hidden % 8 != 0)) return false;
+  if (hd->vocab_total != 0) {  // vocab shard [offset, offset + vocab) of vocab_total
+    if (hd->vocab_total < 0 || hd->vocab_total >= (int64_t(1) << 31) || hd->vocab_offset < 0 ||
+        hd->vocab_offset + hd->vocab > hd->vocab_total)
+      return false;
+  }
   return true;
 }
 
@@ -139,10 +144,14 @@ rl_status rl_batch_prepare(const rl_head* hd, const rl_batch* b, int32_t* row_se
                         reinterpret_cast<cudaStream_t>(stream));
 }
 
-rl_status rl_logprob_fwd(const rl_head* hd, const void* hidden, const void* weight,
-                         const rl_batch* b, float* logp, float* entropy, float* lse, void* ws,
-                         size_t ws_bytes, rl_stream_t stream) {
-  if (!head_ok(hd) || !batch_ok(b) || !logp || !weight) return RL_ERR_INVALID_ARG;
+}  // extern "C"
+
+// Forward (H1, H3, H4). parts_out == NULL: finish the softmax locally into
+// logp/entropy/lse; else write this vocab shard's merged partials.
+static rl_status fwd_impl(const rl_head* hd, const void* hidden, const void* weight,
+                          const rl_batch* b, float* logp, float* entropy, float* lse,
+                          float* parts_out, void* ws, size_t ws_bytes, rl_stream_t stream) {
+  if (!head_ok(hd) || !batch_ok(b) || !weight || (!logp && !parts_out)) return RL_ERR_INVALID_ARG;
   if (b->num_rows > 0 && !hidden) return RL_ERR_INVALID_ARG;
   WsLayout L;
   ws_layout(hd, b->num_rows, 0, &L);
@@ -168,6 +177,66 @@ rl_status rl_logprob_fwd(const rl_head* hd, const void* hidden, const void* weig
   a.zy = reinterpret_cast<const float*>(w + L.off_zy);
   a.active_idx = reinterpret_cast<const int32_t*>(w + L.off_active);
   a.seq_c = reinterpret_cast<const int32_t*>(w + L.off_seq);
+  if (parts_out) {
+    a.parts_out = parts_out;
+    a.ldo = b->num_rows;
+    a.tgt_c = reinterpret_cast<const int32_t*>(w + L.off_tgt);
+    a.y_off = hd->vocab_total > 0 ? hd->vocab_offset : 0;
+    a.v_shard = hd->vocab;
+  } else {
+    a.logp = logp;
+    a.entropy = entropy;
+    a.lse = lse;
+  }
+  return launch_merge(L, w, a, s);
+}
+
+// MergeArgs reading P gathered shard partials parts_all [P][4][R].
+static void gathered_parts(MergeArgs& a, const float* parts_all, int32_t nparts, int64_t R,
+                           const WsLayout& L, char* w) {
+  a.pm = parts_all;
+  a.ps = parts_all + R;
+  a.pu = parts_all + 2 * R;
+  a.nparts = nparts;
+  a.part_stride = 4 * R;
+  a.zy = reinterpret_cast<const float*>(w + L.off_zy);  // filled by launch_zy_combine
+  a.active_idx = reinterpret_cast<const int32_t*>(w + L.off_active);
+  a.seq_c = reinterpret_cast<const int32_t*>(w + L.off_seq);
+}
+
+extern "C" {
+
+rl_status rl_logprob_fwd(const rl_head* hd, const void* hidden, const void* weight,
+                         const rl_batch* b, float* logp, float* entropy, float* lse, void* ws,
+                         size_t ws_bytes, rl_stream_t stream) {
+  if (!logp) return RL_ERR_INVALID_ARG;
+  return fwd_impl(hd, hidden, weight, b, logp, entropy, lse, nullptr, ws, ws_bytes, stream);
+}
+
+rl_status rl_logprob_partials(const rl_head* hd, const void* hidden, const void* weight,
+                              const rl_batch* b, float* parts, void* ws, size_t ws_bytes,
+                              rl_stream_t stream) {
+  if (!parts) return RL_ERR_INVALID_ARG;
+  return fwd_impl(hd, hidden, weight, b, nullptr, nullptr, nullptr, parts, ws, ws_bytes, stream);
+}
+
+rl_status rl_logprob_merge(const rl_head* hd, const rl_batch* b, const float* parts_all,
+                           int32_t nparts, float* logp, float* entropy, float* lse, void* ws,
+                           size_t ws_bytes, rl_stream_t stream) {
+  if (!head_ok(hd) || !batch_ok(b) || !logp || nparts < 1) return RL_ERR_INVALID_ARG;
+  if (b->num_rows > 0 && !parts_all) return RL_ERR_INVALID_ARG;
+  WsLayout L;
+  ws_layout(hd, b->num_rows, 0, &L);
+  if (!ws || ws_bytes < L.total) return RL_ERR_WORKSPACE;
+  if (!aligned(ws, 256)) return RL_ERR_INVALID_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  char* w = static_cast<char*>(ws);
+  rl_status st = launch_prepare(hd, b, L, w, nullptr, nullptr, nullptr, nullptr, nullptr, logp,
+                                entropy, lse, s);
+  if (st != RL_OK) return st;
+  if ((st = launch_zy_combine(parts_all, nparts, b->num_rows, L, w, s)) != RL_OK) return st;
+  MergeArgs a{};
+  gathered_parts(a, parts_all, nparts, b->num_rows, L, w);
   a.logp = logp;
   a.entropy = entropy;
   a.lse = lse;
@@ -196,13 +265,19 @@ rl_status rl_grpo_advantage(const float* rewards, const int32_t* group_of_seq, i
                      reinterpret_cast<cudaStream_t>(stream));
 }
 
-rl_status rl_policy_loss_fwd_bwd(const rl_head* hd, const void* hidden, const void* weight,
-                                 const rl_batch* b, const float* old_logp, const float* adv,
-                                 const rl_loss_params* p, float* logp, float* entropy,
-                                 void* grad_hidden, float* grad_weight, rl_loss_stats* stats,
-                                 void* ws, size_t ws_bytes, rl_stream_t stream) {
+}  // extern "C"
+
+// Training-worker path (H1-H8). parts_all == NULL: the softmax is finished
+// from this call's own forward GEMM; else (vocab-parallel) from the P
+// gathered shard partials, and the backward covers this shard only.
+static rl_status loss_impl(const rl_head* hd, const void* hidden, const void* weight,
+                           const rl_batch* b, const float* parts_all, int32_t nparts,
+                           const float* old_logp, const float* adv, const rl_loss_params* p,
+                           float* logp, float* entropy, void* grad_hidden, float* grad_weight,
+                           rl_loss_stats* stats, void* ws, size_t ws_bytes, rl_stream_t stream) {
   if (!head_ok(hd) || !batch_ok(b) || !weight || !p || !logp || !grad_weight)
     return RL_ERR_INVALID_ARG;
+  if (parts_all && nparts < 1) return RL_ERR_INVALID_ARG;
   if (b->num_rows > 0 && (!hidden || !old_logp || !grad_hidden)) return RL_ERR_INVALID_ARG;
   if (b->num_seqs > 0 && !adv) return RL_ERR_INVALID_ARG;
   if (!(p->clip_lo >= 0.f) || !(p->clip_lo < 1.f) || !(p->clip_hi >= 0.f) ||
@@ -227,19 +302,24 @@ rl_status rl_policy_loss_fwd_bwd(const rl_head* hd, const void* hidden, const vo
                                 entropy, nullptr, s);
   if (st != RL_OK) return st;
   if ((st = launch_zero_inactive(hd, grad_hidden, L, w, s)) != RL_OK) return st;
-  if (tc) {
-    if ((st = launch_gather_bf16(hd, hidden, L, w, s)) != RL_OK) return st;
-    if ((st = launch_tc_fwd(hd, weight, L, w, s)) != RL_OK) return st;
-  } else {
-    if ((st = launch_simt_fwd(hd, hidden, weight, L, w, s)) != RL_OK) return st;
-  }
+  if (tc && (st = launch_gather_bf16(hd, hidden, L, w, s)) != RL_OK) return st;
   MergeArgs a{};
-  a.pm = reinterpret_cast<const float*>(w + L.off_pm);
-  a.ps = reinterpret_cast<const float*>(w + L.off_ps);
-  a.pu = reinterpret_cast<const float*>(w + L.off_pu);
-  a.zy = reinterpret_cast<const float*>(w + L.off_zy);
-  a.active_idx = reinterpret_cast<const int32_t*>(w + L.off_active);
-  a.seq_c = reinterpret_cast<const int32_t*>(w + L.off_seq);
+  if (parts_all) {
+    if ((st = launch_zy_combine(parts_all, nparts, b->num_rows, L, w, s)) != RL_OK) return st;
+    gathered_parts(a, parts_all, nparts, b->num_rows, L, w);
+  } else {
+    if (tc) {
+      if ((st = launch_tc_fwd(hd, weight, L, w, s)) != RL_OK) return st;
+    } else {
+      if ((st = launch_simt_fwd(hd, hidden, weight, L, w, s)) != RL_OK) return st;
+    }
+    a.pm = reinterpret_cast<const float*>(w + L.off_pm);
+    a.ps = reinterpret_cast<const float*>(w + L.off_ps);
+    a.pu = reinterpret_cast<const float*>(w + L.off_pu);
+    a.zy = reinterpret_cast<const float*>(w + L.off_zy);
+    a.active_idx = reinterpret_cast<const int32_t*>(w + L.off_active);
+    a.seq_c = reinterpret_cast<const int32_t*>(w + L.off_seq);
+  }
   a.logp = logp;
   a.entropy = entropy;
   a.lse = nullptr;
@@ -268,6 +348,29 @@ rl_status rl_policy_loss_fwd_bwd(const rl_head* hd, const void* hidden, const vo
   if ((st = launch_stats_reduce(L, w, stats, s)) != RL_OK) return st;
   if (tc) return launch_tc_bwd(hd, weight, grad_hidden, grad_weight, entropy_on, L, w, s);
   return launch_simt_bwd(hd, hidden, weight, grad_hidden, grad_weight, entropy_on, L, w, s);
+}
+
+extern "C" {
+
+rl_status rl_policy_loss_fwd_bwd(const rl_head* hd, const void* hidden, const void* weight,
+                                 const rl_batch* b, const float* old_logp, const float* adv,
+                                 const rl_loss_params* p, float* logp, float* entropy,
+                                 void* grad_hidden, float* grad_weight, rl_loss_stats* stats,
+                                 void* ws, size_t ws_bytes, rl_stream_t stream) {
+  return loss_impl(hd, hidden, weight, b, nullptr, 0, old_logp, adv, p, logp, entropy,
+                   grad_hidden, grad_weight, stats, ws, ws_bytes, stream);
+}
+
+rl_status rl_policy_loss_fwd_bwd_vp(const rl_head* hd, const void* hidden, const void* weight,
+                                    const rl_batch* b, const float* parts_all, int32_t nparts,
+                                    const float* old_logp, const float* adv,
+                                    const rl_loss_params* p, float* logp, float* entropy,
+                                    void* grad_hidden, float* grad_weight, rl_loss_stats* stats,
+                                    void* ws, size_t ws_bytes, rl_stream_t stream) {
+  if (b && b->num_rows > 0 && !parts_all) return RL_ERR_INVALID_ARG;
+  if (nparts < 1) return RL_ERR_INVALID_ARG;
+  return loss_impl(hd, hidden, weight, b, parts_all, nparts, old_logp, adv, p, logp, entropy,
+                   grad_hidden, grad_weight, stats, ws, ws_bytes, stream);
 }
 
 const char* rl_status_string(rl_status s) {

@@ -33,6 +33,11 @@ constexpr int TC_BM = 128;   // rows per tcgen05 tile (UMMA M)
 constexpr int TC_BN = 256;   // columns per tile (UMMA N)
 constexpr int TC_BK = 64;    // K per pipeline stage (one 128-B swizzle row)
 
+// Vocabulary of the whole (possibly vocab-sharded) head; targets live in it.
+inline int64_t vocab_total(const rl_head* hd) {
+  return hd->vocab_total > 0 ? hd->vocab_total : hd->vocab;
+}
+
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
 

@@ -27,9 +27,16 @@ rl_status launch_grpo(const float* rewards, const int32_t* gos, int32_t S, int32
 
 // H4 merge of the split-V partials (+ H5 loss when old_logp != NULL).
 struct MergeArgs {
-  const float *pm, *ps, *pu, *zy;
+  const float *pm, *ps, *pu, *zy;       // partial n of compact row r at [n * part_stride + r]
+  int64_t nparts, part_stride;
   const int32_t *active_idx, *seq_c;
   float *logp, *entropy, *lse;          // row space, may be NULL
+  // vocab-parallel phase 1: write this shard's merged (m, s, u, zy-or-0) to
+  // parts_out[k * ldo + r] instead of logp/entropy/lse
+  float* parts_out;
+  int64_t ldo;
+  const int32_t* tgt_c;
+  int64_t y_off, v_shard;
   // loss
   const float* old_logp;                // row space; NULL = fwd only
   const float* adv;                     // per sequence
@@ -49,6 +56,9 @@ struct MergeArgs {
   long long* st_i;                      // [nblk][3] clip_lo, clip_hi, tokens
 };
 rl_status launch_merge(const WsLayout& L, char* ws, const MergeArgs& a, cudaStream_t s);
+// zy[r] = sum_p parts_all[p][3][r] (exactly one shard holds the target).
+rl_status launch_zy_combine(const float* parts_all, int64_t nparts, int64_t ldr,
+                            const WsLayout& L, char* ws, cudaStream_t s);
 rl_status launch_stats_reduce(const WsLayout& L, char* ws, rl_loss_stats* stats, cudaStream_t s);
 
 // CUDA-core path (fp32 exact; also bf16 for cross-checks).

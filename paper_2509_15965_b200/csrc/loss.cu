@@ -75,14 +75,15 @@ __device__ __forceinline__ int64_t lower_bound_rows(const int32_t* __restrict__ 
 
 template <bool LOSS>
 __global__ void __launch_bounds__(MERGE_THREADS)
-k_merge(MergeArgs a, const WsHeader* __restrict__ hdr, int64_t n_vt, int64_t ldp) {
+k_merge(MergeArgs a, const WsHeader* __restrict__ hdr, int64_t ldp) {
   const int64_t T = hdr->n_active;
   const int64_t r = static_cast<int64_t>(blockIdx.x) * MERGE_THREADS + threadIdx.x;
+  const int64_t n_vt = a.nparts, pst = a.part_stride;
   LStat st{0.0, 0.0, 0.0, 0.0, 0.0, 0.f, 0, 0, 0};
   if (r < T) {
     float M = a.pm[r], S = a.ps[r], U = a.pu[r];
     for (int64_t n = 1; n < n_vt; ++n) {
-      const float m = a.pm[n * ldp + r], s = a.ps[n * ldp + r], u = a.pu[n * ldp + r];
+      const float m = a.pm[n * pst + r], s = a.ps[n * pst + r], u = a.pu[n * pst + r];
       if (m > M) {  // rescale the running sums to the new max
         const float f = expf(M - m);
         U = f * (U + (M - m) * S);
@@ -92,6 +93,14 @@ k_merge(MergeArgs a, const WsHeader* __restrict__ hdr, int64_t n_vt, int64_t ldp
       const float f2 = expf(m - M);
       S += s * f2;
       U += f2 * (u + (m - M) * s);
+    }
+    if (a.parts_out) {  // vocab-parallel phase 1: this shard's merged partial
+      const int64_t yl = static_cast<int64_t>(a.tgt_c[r]) - a.y_off;
+      a.parts_out[r] = M;
+      a.parts_out[a.ldo + r] = S;
+      a.parts_out[2 * a.ldo + r] = U;
+      a.parts_out[3 * a.ldo + r] = (yl >= 0 && yl < a.v_shard) ? a.zy[r] : 0.f;
+      return;
     }
     const float logS = logf(S);
     const float lse = M + logS;
@@ -178,16 +187,41 @@ k_merge(MergeArgs a, const WsHeader* __restrict__ hdr, int64_t n_vt, int64_t ldp
   }
 }
 
-rl_status launch_merge(const WsLayout& L, char* ws, const MergeArgs& a, cudaStream_t s) {
+rl_status launch_merge(const WsLayout& L, char* ws, const MergeArgs& a_in, cudaStream_t s) {
   const WsHeader* hdr = reinterpret_cast<const WsHeader*>(ws + L.off_hdr);
   if (L.nblk_loss == 0) return RL_OK;
+  MergeArgs a = a_in;
+  if (a.nparts == 0) {  // this call's own split-V partials in the workspace
+    a.nparts = L.n_vt;
+    a.part_stride = L.Rp;
+  }
+  if (a.parts_out && a.old_logp) return RL_ERR_INVALID_ARG;
   TraceScope ts(RL_K_MERGE, s);
   if (a.old_logp)
-    k_merge<true><<<static_cast<unsigned>(L.nblk_loss), MERGE_THREADS, 0, s>>>(a, hdr, L.n_vt,
-                                                                                L.Rp);
+    k_merge<true><<<static_cast<unsigned>(L.nblk_loss), MERGE_THREADS, 0, s>>>(a, hdr, L.Rp);
   else
-    k_merge<false><<<static_cast<unsigned>(L.nblk_loss), MERGE_THREADS, 0, s>>>(a, hdr, L.n_vt,
-                                                                                 L.Rp);
+    k_merge<false><<<static_cast<unsigned>(L.nblk_loss), MERGE_THREADS, 0, s>>>(a, hdr, L.Rp);
+  RLH_CHECK_LAUNCH();
+  return RL_OK;
+}
+
+__global__ void __launch_bounds__(MERGE_THREADS)
+k_zy_combine(const float* __restrict__ parts_all, int64_t nparts, int64_t ldr,
+             const WsHeader* __restrict__ hdr, float* __restrict__ zy) {
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * MERGE_THREADS + threadIdx.x;
+  if (r >= hdr->n_active) return;
+  float acc = 0.f;  // one shard holds z_y, the others contribute exact zeros
+  for (int64_t p = 0; p < nparts; ++p) acc += parts_all[(4 * p + 3) * ldr + r];
+  zy[r] = acc;
+}
+
+rl_status launch_zy_combine(const float* parts_all, int64_t nparts, int64_t ldr,
+                            const WsLayout& L, char* ws, cudaStream_t s) {
+  if (L.nblk_loss == 0) return RL_OK;
+  TraceScope ts(RL_K_MERGE, s);
+  k_zy_combine<<<static_cast<unsigned>(L.nblk_loss), MERGE_THREADS, 0, s>>>(
+      parts_all, nparts, ldr, reinterpret_cast<const WsHeader*>(ws + L.off_hdr),
+      reinterpret_cast<float*>(ws + L.off_zy));
   RLH_CHECK_LAUNCH();
   return RL_OK;
 }

@@ -191,7 +191,8 @@ rl_status launch_prepare(const rl_head* hd, const rl_batch* b, const WsLayout& L
   if (nblk > 0) {
     TraceScope ts(RL_K_PREPARE, s);
     k_flags<<<static_cast<unsigned>(nblk), PREP_THREADS, 0, s>>>(
-        b->cu_seqlens, b->num_seqs, R, b->targets, b->mask, hd->vocab, hdr, act, row_seq, blk_cnt,
+        b->cu_seqlens, b->num_seqs, R, b->targets, b->mask,
+        static_cast<int32_t>(vocab_total(hd)), hdr, act, row_seq, blk_cnt,
         zero0, zero1, zero2, b->err_flags);
   }
   RLH_CHECK_LAUNCH();

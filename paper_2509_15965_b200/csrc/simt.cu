@@ -45,7 +45,7 @@ __device__ __forceinline__ MSU msu_merge(MSU a, MSU b) {
 template <typename T>
 __global__ void __launch_bounds__(SIMT_THREADS)
 k_simt_fwd(const T* __restrict__ hidden, int64_t ld, const T* __restrict__ W, int h, int V,
-           float inv_temp, const int32_t* __restrict__ active_idx,
+           float inv_temp, int64_t y_off, const int32_t* __restrict__ active_idx,
            const int32_t* __restrict__ tgt_c, const WsHeader* __restrict__ hdr,
            float* __restrict__ pm, float* __restrict__ ps, float* __restrict__ pu,
            float* __restrict__ zy) {
@@ -56,7 +56,7 @@ k_simt_fwd(const T* __restrict__ hidden, int64_t ld, const T* __restrict__ W, in
     const T* hrow = hidden + static_cast<int64_t>(active_idx[r]) * ld;
     for (int k = threadIdx.x; k < h; k += SIMT_THREADS) hs[k] = to_f(hrow[k]);
     __syncthreads();
-    const int y = tgt_c[r];
+    const int64_t y = static_cast<int64_t>(tgt_c[r]) - y_off;  // local id in this shard
     MSU acc{-INFINITY, 0.f, 0.f};
     for (int v = threadIdx.x; v < V; v += SIMT_THREADS) {
       const float z = simt_logit(hs, W + static_cast<int64_t>(v) * h, h, inv_temp);
@@ -81,7 +81,7 @@ k_simt_fwd(const T* __restrict__ hidden, int64_t ld, const T* __restrict__ W, in
 template <typename T>
 __global__ void __launch_bounds__(SIMT_THREADS)
 k_simt_dz(const T* __restrict__ hidden, int64_t ld, const T* __restrict__ W, int h, int V,
-          float inv_temp, const int32_t* __restrict__ active_idx,
+          float inv_temp, int64_t y_off, const int32_t* __restrict__ active_idx,
           const int32_t* __restrict__ tgt_c, const WsHeader* __restrict__ hdr,
           const float* __restrict__ lse_c, const float* __restrict__ g_c,
           const float* __restrict__ ge_c, const float* __restrict__ ez_c,
@@ -92,7 +92,7 @@ k_simt_dz(const T* __restrict__ hidden, int64_t ld, const T* __restrict__ W, int
     const T* hrow = hidden + static_cast<int64_t>(active_idx[r]) * ld;
     for (int k = threadIdx.x; k < h; k += SIMT_THREADS) hs[k] = to_f(hrow[k]);
     __syncthreads();
-    const int y = tgt_c[r];
+    const int64_t y = static_cast<int64_t>(tgt_c[r]) - y_off;  // local id in this shard
     const float lse = lse_c[r], coef = g_c[r] * inv_temp;
     const float cent = ge_c ? ge_c[r] * inv_temp : 0.f, ez = ge_c ? ez_c[r] : 0.f;
     for (int v = threadIdx.x; v < V; v += SIMT_THREADS) {
@@ -192,7 +192,8 @@ static rl_status simt_fwd_t(const rl_head* hd, const void* hidden, const void* w
   TraceScope ts(RL_K_SIMT_FWD, s);
   k_simt_fwd<T><<<blocks, SIMT_THREADS, smem, s>>>(
       static_cast<const T*>(hidden), hd->ld_hidden, static_cast<const T*>(weight), hd->hidden,
-      hd->vocab, hd->inv_temperature, reinterpret_cast<const int32_t*>(ws + L.off_active),
+      hd->vocab, hd->inv_temperature, hd->vocab_total > 0 ? hd->vocab_offset : 0,
+      reinterpret_cast<const int32_t*>(ws + L.off_active),
       reinterpret_cast<const int32_t*>(ws + L.off_tgt), hdr,
       reinterpret_cast<float*>(ws + L.off_pm), reinterpret_cast<float*>(ws + L.off_ps),
       reinterpret_cast<float*>(ws + L.off_pu), reinterpret_cast<float*>(ws + L.off_zy));
@@ -219,7 +220,8 @@ static rl_status simt_bwd_t(const rl_head* hd, const void* hidden, const void* w
     TraceScope ts(RL_K_SIMT_BWD, s);
     k_simt_dz<T><<<blocks, SIMT_THREADS, smem, s>>>(
         static_cast<const T*>(hidden), hd->ld_hidden, static_cast<const T*>(weight), h, V,
-        hd->inv_temperature, active_idx, reinterpret_cast<const int32_t*>(ws + L.off_tgt), hdr,
+        hd->inv_temperature, hd->vocab_total > 0 ? hd->vocab_offset : 0, active_idx,
+        reinterpret_cast<const int32_t*>(ws + L.off_tgt), hdr,
         reinterpret_cast<const float*>(ws + L.off_lse), reinterpret_cast<const float*>(ws + L.off_g),
         entropy_on ? reinterpret_cast<const float*>(ws + L.off_ge) : nullptr,
         entropy_on ? reinterpret_cast<const float*>(ws + L.off_ez) : nullptr, dz);

@@ -72,7 +72,8 @@ struct TcArgs {
   int32_t l2_policy;   // TMA L2 hint: 0 normal, 1 evict_last, 2 evict_first
   const WsHeader* hdr;
   float inv_temp;
-  int32_t vocab;
+  int32_t vocab;       // columns of this (shard of the) head
+  int64_t y_off;       // global id of column 0 (vocab-parallel shard offset)
   // EPI_LSE
   float *pm, *ps, *pu, *zy;
   const int32_t* tgt_c;
@@ -281,8 +282,9 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + static_cast<uint32_t>(acc * TC_BN);
 
       if constexpr (EPI == EPI_LSE) {
-        const int y = row_ok ? args.tgt_c[row] : -1;
-        const int yrel = y - n0;
+        // target column in this shard (or none): local id = global - y_off
+        const int64_t yl = row_ok ? static_cast<int64_t>(args.tgt_c[row]) - args.y_off : -1;
+        const int yrel = (yl >= 0 && yl < args.vocab) ? static_cast<int>(yl) - n0 : -(1 << 30);
         const int valid = args.vocab - n0;  // columns < valid are real vocab ids
         float m = -INFINITY, s = 0.f, u = 0.f, zyv = 0.f;
         bool has_y = false;
@@ -338,7 +340,8 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       } else if constexpr (EPI == EPI_DZ) {
         const float lse = row_ok ? args.lse_c[row] : 0.f;
         const float coef = row_ok ? args.g_c[row] * args.inv_temp : 0.f;
-        const int yrel = (row_ok ? args.tgt_c[row] : -1) - n0;
+        const int64_t yl = row_ok ? static_cast<int64_t>(args.tgt_c[row]) - args.y_off : -1;
+        const int yrel = (yl >= 0 && yl < args.vocab) ? static_cast<int>(yl) - n0 : -(1 << 30);
         const float lse2 = lse * LOG2E, sc2 = args.inv_temp * LOG2E;
         uint4* dst = reinterpret_cast<uint4*>(args.dz + row * args.ld_dz + n0);
         const uint64_t st_pol = l2_policy_evict_first();  // 17 GB stream: keep W/Hc in L2
@@ -571,6 +574,7 @@ static TcArgs base_args(const rl_head* hd, const WsLayout& L, char* ws) {
   t.hdr = reinterpret_cast<const WsHeader*>(ws + L.off_hdr);
   t.inv_temp = hd->inv_temperature;
   t.vocab = hd->vocab;
+  t.y_off = hd->vocab_total > 0 ? hd->vocab_offset : 0;
   t.l2_policy = env_int("RLHEAD_L2_POLICY", 1);
   t.tgt_c = reinterpret_cast<const int32_t*>(ws + L.off_tgt);
   t.ldp = L.Rp;

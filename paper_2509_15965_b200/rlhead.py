@@ -34,7 +34,8 @@ class rl_batch(C.Structure):
 
 class rl_head(C.Structure):
     _fields_ = [("hidden", C.c_int32), ("vocab", C.c_int32), ("dtype", C.c_int),
-                ("ld_hidden", C.c_int64), ("inv_temperature", C.c_float)]
+                ("ld_hidden", C.c_int64), ("inv_temperature", C.c_float),
+                ("vocab_offset", C.c_int64), ("vocab_total", C.c_int64)]
 
 
 class rl_loss_params(C.Structure):
@@ -70,6 +71,16 @@ lib.rl_policy_loss_fwd_bwd.restype = C.c_int
 lib.rl_policy_loss_fwd_bwd.argtypes = [C.POINTER(rl_head), _vp, _vp, C.POINTER(rl_batch), _vp,
                                        _vp, C.POINTER(rl_loss_params), _vp, _vp, _vp, _vp, _vp,
                                        _vp, _sz, _vp]
+lib.rl_logprob_partials.restype = C.c_int
+lib.rl_logprob_partials.argtypes = [C.POINTER(rl_head), _vp, _vp, C.POINTER(rl_batch), _vp, _vp,
+                                    _sz, _vp]
+lib.rl_logprob_merge.restype = C.c_int
+lib.rl_logprob_merge.argtypes = [C.POINTER(rl_head), C.POINTER(rl_batch), _vp, C.c_int32, _vp,
+                                 _vp, _vp, _vp, _sz, _vp]
+lib.rl_policy_loss_fwd_bwd_vp.restype = C.c_int
+lib.rl_policy_loss_fwd_bwd_vp.argtypes = [C.POINTER(rl_head), _vp, _vp, C.POINTER(rl_batch), _vp,
+                                          C.c_int32, _vp, _vp, C.POINTER(rl_loss_params), _vp,
+                                          _vp, _vp, _vp, _vp, _vp, _sz, _vp]
 lib.rl_status_string.restype = C.c_char_p
 lib.rl_status_string.argtypes = [C.c_int]
 lib.rl_build_info.restype = C.c_char_p
@@ -83,7 +94,8 @@ lib.rl_trace_durations.argtypes = [_vp, C.c_int32]
 
 EXPORTED = ["rl_workspace_size", "rl_batch_prepare", "rl_logprob_fwd", "rl_grpo_group_stats",
             "rl_grpo_advantage", "rl_policy_loss_fwd_bwd", "rl_status_string", "rl_build_info",
-            "rl_launch_count", "rl_trace_begin", "rl_trace_end", "rl_trace_durations"]
+            "rl_launch_count", "rl_trace_begin", "rl_trace_end", "rl_trace_durations",
+            "rl_logprob_partials", "rl_logprob_merge", "rl_policy_loss_fwd_bwd_vp"]
 
 
 class RLHeadError(RuntimeError):
@@ -112,14 +124,17 @@ def _stream(stream=None):
 class Head:
     """rl_head: hidden size h, vocab V, dtype ('bf16' | 'f32'), ld_hidden, 1/tau."""
     hidden: int
-    vocab: int
+    vocab: int                 # rows of the weight passed with this head (a shard if sharded)
     dtype: str = "bf16"
     ld_hidden: int | None = None
     inv_temperature: float = 1.0
+    vocab_offset: int = 0      # vocab-parallel shard: first global id of `vocab` rows
+    vocab_total: int = 0       # 0 = unsharded
 
     def c(self) -> rl_head:
         return rl_head(self.hidden, self.vocab, RL_BF16 if self.dtype == "bf16" else RL_F32,
-                       self.ld_hidden or self.hidden, self.inv_temperature)
+                       self.ld_hidden or self.hidden, self.inv_temperature, self.vocab_offset,
+                       self.vocab_total)
 
 
 @dataclass
@@ -242,6 +257,44 @@ def rl_policy_loss_fwd_bwd(head: Head, hidden, weight, batch: Batch, old_logp, a
                                       _ptr(entropy), _ptr(grad_hidden), _ptr(grad_weight),
                                       _ptr(stats), _ptr(buf), buf.numel(), _stream(stream)),
            "rl_policy_loss_fwd_bwd")
+
+
+def rl_logprob_partials(head: Head, hidden, weight, batch: Batch, parts,
+                        ws: Workspace | None = None, stream=None):
+    """Vocab-parallel phase 1: this shard's merged partials, parts fp32 [4, R]."""
+    hd, b = head.c(), batch.c()
+    ws = ws or Workspace()
+    buf = ws.get(rl_workspace_size(head, b.num_rows, False))
+    _check(lib.rl_logprob_partials(C.byref(hd), _ptr(hidden), _ptr(weight), C.byref(b),
+                                   _ptr(parts), _ptr(buf), buf.numel(), _stream(stream)),
+           "rl_logprob_partials")
+
+
+def rl_logprob_merge(head: Head, batch: Batch, parts_all, logp, entropy=None, lse=None,
+                     ws: Workspace | None = None, stream=None):
+    """Vocab-parallel phase 2 (inference): parts_all fp32 [P, 4, R] -> logp etc."""
+    hd, b = head.c(), batch.c()
+    ws = ws or Workspace()
+    buf = ws.get(rl_workspace_size(head, b.num_rows, False))
+    _check(lib.rl_logprob_merge(C.byref(hd), C.byref(b), _ptr(parts_all), int(parts_all.shape[0]),
+                                _ptr(logp), _ptr(entropy), _ptr(lse), _ptr(buf), buf.numel(),
+                                _stream(stream)), "rl_logprob_merge")
+
+
+def rl_policy_loss_fwd_bwd_vp(head: Head, hidden, weight, batch: Batch, parts_all, old_logp, adv,
+                              params: LossParams, logp, grad_hidden, grad_weight, entropy=None,
+                              stats=None, ws: Workspace | None = None, stream=None):
+    """Vocab-parallel phase 2 (training): grad_hidden is this shard's partial
+    dL/dH (all-reduce SUM over the TP group), grad_weight its rows of dL/dW."""
+    hd, b, p = head.c(), batch.c(), params.c()
+    ws = ws or Workspace()
+    buf = ws.get(rl_workspace_size(head, b.num_rows, True))
+    _check(lib.rl_policy_loss_fwd_bwd_vp(C.byref(hd), _ptr(hidden), _ptr(weight), C.byref(b),
+                                         _ptr(parts_all), int(parts_all.shape[0]), _ptr(old_logp),
+                                         _ptr(adv), C.byref(p), _ptr(logp), _ptr(entropy),
+                                         _ptr(grad_hidden), _ptr(grad_weight), _ptr(stats),
+                                         _ptr(buf), buf.numel(), _stream(stream)),
+           "rl_policy_loss_fwd_bwd_vp")
 
 
 def rl_launch_count() -> int:

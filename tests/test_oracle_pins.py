@@ -432,3 +432,44 @@ def test_loss_scale_streaming_mode():
     b = oracle.policy_loss_fwd_bwd(H, W, cu, mask, y, old, adv,
                                    oracle.LossParams(loss_scale=1.0))
     np.testing.assert_allclose(b["dW"] / a["n_active"], a["dW"], atol=1e-15)
+
+
+# ------------------------------------------------------------- NEXT-3 -------
+@pytest.mark.parametrize("cuts", [[0, 1000], [0, 333, 666, 1000], [0, 1, 999, 1000],
+                                  [0, 512, 1000]])
+def test_vocab_partition_merge_equals_full_softmax(cuts):
+    """Vocab-parallel pin: merging shard partials over ANY partition of the
+    vocabulary equals the unsharded log-softmax (associativity of logsumexp;
+    the merge is written in a different form from the oracle's forward)."""
+    rng = np.random.default_rng(len(cuts))
+    R, h, V = 30, 8, 1000
+    H = rng.normal(size=(R, h))
+    W = rng.normal(scale=1.5, size=(V, h))
+    y = rng.integers(0, V, size=R).astype(np.int32)
+    cu, m = _flat_batch(R)
+    full = oracle.logprob_fwd(H, W, cu, m, y, inv_temperature=1.3)
+    parts = [oracle.head.logprob_shard_partials(H, W[a:b], a, V, cu, m, y, inv_temperature=1.3)
+             for a, b in zip(cuts[:-1], cuts[1:])]
+    mg = oracle.head.merge_shard_partials(np.stack(parts))
+    np.testing.assert_allclose(mg["logp"], full["logp"], atol=1e-12)
+    np.testing.assert_allclose(mg["entropy"], full["entropy"], atol=1e-12)
+    np.testing.assert_allclose(mg["lse"], full["lse"], atol=1e-12)
+
+
+def test_vocab_shard_partials_mpmath():
+    """One shard's (m, s, u, zy) against 50-digit brute force."""
+    mpmath.mp.dps = 50
+    H, W, y = _rand_problem(R=3, h=4, V=9, seed=11, scale=2.0)
+    y[:] = [2, 7, 5]
+    cu, m = _flat_batch(3)
+    p = oracle.head.logprob_shard_partials(H, W[4:9], 4, 9, cu, m, y)
+    for t in range(3):
+        z = [mpmath.fsum(mpmath.mpf(H[t, k]) * mpmath.mpf(W[j, k]) for k in range(4))
+             for j in range(4, 9)]
+        mx = max(z)
+        s = mpmath.fsum(mpmath.exp(zj - mx) for zj in z)
+        u = mpmath.fsum(mpmath.exp(zj - mx) * (zj - mx) for zj in z)
+        assert p[0, t] == pytest.approx(float(mx), abs=1e-13)
+        assert p[1, t] == pytest.approx(float(s), rel=1e-13)
+        assert p[2, t] == pytest.approx(float(u), rel=1e-12, abs=1e-13)
+        assert p[3, t] == (0.0 if y[t] < 4 else pytest.approx(float(z[y[t] - 4]), abs=1e-13))

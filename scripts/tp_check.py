@@ -1,0 +1,91 @@
+#!/usr/bin/env python
+"""Vocab-parallel head across real GPUs (NEXT-3): every rank holds one vocab
+shard of the head; rank 0 also runs the unsharded head on its GPU and compares.
+
+    torchrun --nproc-per-node 2 scripts/tp_check.py [--config qwen7b --rows 16384]
+
+Prints one JSON line: max |dlogp| vs unsharded, relative dH / dW differences,
+and the TP micro-batch time (CUDA events, max over ranks)."""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="qwen7b")
+    ap.add_argument("--rows", type=int, default=16384)
+    ap.add_argument("--reps", type=int, default=3)
+    a = ap.parse_args()
+    import torch
+    import torch.distributed as dist
+
+    import paper_2509_15965_b200 as rl
+    from paper_2509_15965_b200.dp import pack_micro_batches
+    from paper_2509_15965_b200.tp import VocabParallelHead, vocab_shards
+    from workload import CONFIGS, make_layout, make_tensors_torch, sub_layout
+    rank, world, local = (int(os.environ.get(k, d)) for k, d in
+                          (("RANK", 0), ("WORLD_SIZE", 1), ("LOCAL_RANK", 0)))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    cfg = CONFIGS[a.config]
+    lay = make_layout(cfg, 0)
+    cu = lay.cu_seqlens.astype(np.int64)
+    s0, s1 = pack_micro_batches(cu[1:] - cu[:-1], a.rows)[0]
+    mb, _ = sub_layout(lay, np.arange(s0, s1))
+    H, W = make_tensors_torch(cfg, mb.num_rows, seed=5, device=dev)   # same on every rank
+    off, size = vocab_shards(cfg.vocab, world)[rank]
+    Ws = W[off:off + size].contiguous()
+    vp = VocabParallelHead(cfg.hidden, cfg.vocab, off, size, cfg.dtype)
+    b = rl.Batch(torch.as_tensor(mb.cu_seqlens, device=dev), torch.as_tensor(mb.targets, device=dev),
+                 torch.as_tensor(mb.mask, device=dev))
+    Rn = mb.num_rows
+    old = torch.zeros(Rn, device=dev)
+    adv = torch.linspace(-1, 1, mb.num_seqs, device=dev)
+    p = rl.LossParams(n_tokens_global=torch.tensor([mb.num_tokens], device=dev))
+    logp = torch.empty(Rn, device=dev)
+    gh = torch.empty_like(H)
+    gw = torch.zeros(size, cfg.hidden, device=dev)
+    ws = rl.Workspace(dev)
+    vp.loss_fwd_bwd(H, Ws, b, old, adv, p, logp, gh, gw, ws=ws)   # warm-up
+    gw.zero_()
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(a.reps):
+        vp.loss_fwd_bwd(H, Ws, b, old, adv, p, logp, gh, gw, ws=ws)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = torch.tensor([e0.elapsed_time(e1) / a.reps], device=dev, dtype=torch.float64)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    gw /= a.reps
+    # gather the dW shards on rank 0 and compare with the unsharded head there
+    shards = [torch.empty(s, cfg.hidden, device=dev) for _, s in vocab_shards(cfg.vocab, world)]
+    dist.all_gather(shards, gw)
+    if rank == 0:
+        head = rl.Head(cfg.hidden, cfg.vocab, cfg.dtype)
+        lp1 = torch.empty(Rn, device=dev)
+        gh1 = torch.empty_like(H)
+        gw1 = torch.zeros(cfg.vocab, cfg.hidden, device=dev)
+        rl.rl_policy_loss_fwd_bwd(head, H, W, b, old, adv, p, lp1, gh1, gw1, ws=ws)
+        torch.cuda.synchronize()
+        dW = torch.cat(shards)
+        rel = lambda x, y: float((x.double() - y.double()).norm() / y.double().norm())  # noqa: E731
+        print(json.dumps({"tp": world, "config": a.config, "tokens": mb.num_tokens,
+                          "max_dlogp": float((logp - lp1).abs().max()),
+                          "rel_dH": rel(gh, gh1), "rel_dW": rel(dW, gw1),
+                          "ms_per_microbatch": round(float(ms.item()), 3),
+                          "tokens_per_s": round(mb.num_tokens / (float(ms.item()) / 1e3), 1)}))
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -119,3 +119,15 @@ def test_gloo_world2_matches_whole_batch(tmp_path):
     assert st.loss_sum == pytest.approx(ref["stats"]["loss_sum"], abs=1e-12)
     assert st.tokens == ref["stats"]["tokens"]
     assert st.ratio_max == pytest.approx(ref["stats"]["ratio_max"], rel=1e-6)
+
+
+@given(st.integers(1, 300000), st.integers(1, 8))
+@settings(max_examples=200, deadline=None)
+def test_vocab_shards_cover_and_align(V, P):
+    from paper_2509_15965_b200.tp import vocab_shards
+    if -(-(-(-V // P)) // 256) * 256 * (P - 1) >= V:      # too many shards for this vocab
+        return
+    sh = vocab_shards(V, P)
+    assert sh[0][0] == 0 and sum(s for _, s in sh) == V
+    for (o1, s1), (o2, _) in zip(sh, sh[1:]):
+        assert o2 == o1 + s1 and s1 % 256 == 0

@@ -199,6 +199,21 @@ RL_API rl_status rl_policy_loss_fwd_bwd(const rl_head *hd, const void *hidden, c
                                  void *grad_hidden, float *grad_weight, rl_loss_stats *stats,
                                  void *ws, size_t ws_bytes, rl_stream_t stream);
 
+/* ---- mini-batch update control (NEXT-2) ---------------------------------
+ * rl_minibatch_early_stop: "discard minibatches with too large importance
+ * ratio" (DESIGN.md §3 #29). From the (all-reduced) device stats:
+ * stop = (max_ratio > 0 && ratio_max > max_ratio) ||
+ *        (max_mean_ratio > 0 && tokens > 0 && ratio_sum / tokens > max_mean_ratio);
+ * *stop_flag (device int32) = stop; if stop, grad_weight[0..n) := 0.
+ * rl_scale_by_inverse_count: x[0..n) *= 1/count (0 if count == 0), count a
+ * device int64 -- the deferred 1/N of micro-batches run with loss_scale = 1
+ * before N was known (elastic pipelining). x 16-B aligned. */
+RL_API rl_status rl_minibatch_early_stop(const rl_loss_stats *stats, float max_ratio,
+                                         float max_mean_ratio, int32_t *stop_flag,
+                                         float *grad_weight, int64_t n, rl_stream_t stream);
+RL_API rl_status rl_scale_by_inverse_count(float *x, int64_t n, const int64_t *count,
+                                           rl_stream_t stream);
+
 /* ---- vocab-parallel head (NEXT-3) ----------------------
  * A vocab shard cannot finish the log-sum-exp alone. Phase 1 on every rank:
  *   rl_logprob_partials -> parts [4][num_rows] fp32 for THIS shard, in compact

@@ -431,3 +431,29 @@ def merge_shard_partials(parts):
     lse = M + np.log(S)
     Ez = (np.exp(m - M) * (u + m * s)).sum(axis=0) / S
     return dict(lse=lse, entropy=lse - Ez, logp=zy.sum(axis=0) - lse)
+
+
+# --------------------------------------------------------------------------
+# NEXT-2: minibatch early stop and deferred normalisation.
+# "Minibatch Early-Stop: We discard minibatches with too large importance
+# ratio to stabilize training" (reading #29): the update of a
+# mini-batch is discarded (gradient zeroed) when its largest token ratio
+# exceeds max_ratio, or its token-mean ratio exceeds max_mean_ratio (a
+# threshold <= 0 disables that test). Elastic pipelining lets
+# micro-batches run before N is known: they use loss_scale = 1 and the
+# accumulated gradient is multiplied by 1/N at the end (the loss is linear).
+# --------------------------------------------------------------------------
+def minibatch_early_stop(stats, max_ratio=0.0, max_mean_ratio=0.0):
+    """True if the mini-batch's update is discarded."""
+    if max_ratio > 0 and float(stats["ratio_max"]) > max_ratio:
+        return True
+    if max_mean_ratio > 0 and stats["tokens"] > 0 and \
+            float(stats["ratio_sum"]) / float(stats["tokens"]) > max_mean_ratio:
+        return True
+    return False
+
+
+def scale_by_inverse_count(x, count):
+    """x / count (0 when count == 0): the deferred 1/N of streaming mode."""
+    x = np.asarray(x, dtype=np.float64)
+    return x * (1.0 / count) if count > 0 else np.zeros_like(x)

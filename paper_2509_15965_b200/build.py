@@ -1,6 +1,6 @@
 """Build librlhead.so in-tree with nvcc for sm_100a (no GPU needed).
 
-    python -m paper_2509_15965_b200.build [--verbose]
+    python paper_2509_15965_b200/build.py [--verbose] [--ptxas] [--force]
 
 One nvcc invocation per translation unit (parallel), then one link. The
 library links cudart statically and reaches the driver API
@@ -20,7 +20,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(ROOT, "build")
 LIB = os.path.join(PKG, "librlhead.so")
-SOURCES = ["api.cu", "prepare.cu", "grpo.cu", "loss.cu", "simt.cu", "tc_gemm.cu"]
+SOURCES = ["api.cu", "prepare.cu", "grpo.cu", "loss.cu", "simt.cu", "tc_gemm.cu", "update.cu"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

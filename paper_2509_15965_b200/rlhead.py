@@ -3,8 +3,8 @@
 Every function here has the C name and forwards torch tensors as raw device
 pointers plus the current CUDA stream; all arithmetic runs in the library's
 CUDA kernels. There is no CPU fallback: importing this module fails loudly
-when librlhead.so is missing (build it with ``python -m
-paper_2509_15965_b200.build`` or ``__graft_entry__.build()``).
+when librlhead.so is missing (build it with ``python
+paper_2509_15965_b200/build.py`` or ``__graft_entry__.build()``).
 """
 from __future__ import annotations
 
@@ -16,8 +16,8 @@ import numpy as np
 
 _LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "librlhead.so")
 if not os.path.exists(_LIB_PATH):
-    raise ImportError(f"librlhead.so not built at {_LIB_PATH}; run `python -m "
-                      "paper_2509_15965_b200.build` (no CPU fallback exists)")
+    raise ImportError(f"librlhead.so not built at {_LIB_PATH}; run `python "
+                      "paper_2509_15965_b200/build.py` (no CPU fallback exists)")
 lib = C.CDLL(_LIB_PATH)
 
 RL_OK, RL_ERR_INVALID_ARG, RL_ERR_UNSUPPORTED, RL_ERR_WORKSPACE, RL_ERR_CUDA = range(5)
@@ -81,6 +81,10 @@ lib.rl_policy_loss_fwd_bwd_vp.restype = C.c_int
 lib.rl_policy_loss_fwd_bwd_vp.argtypes = [C.POINTER(rl_head), _vp, _vp, C.POINTER(rl_batch), _vp,
                                           C.c_int32, _vp, _vp, C.POINTER(rl_loss_params), _vp,
                                           _vp, _vp, _vp, _vp, _vp, _sz, _vp]
+lib.rl_minibatch_early_stop.restype = C.c_int
+lib.rl_minibatch_early_stop.argtypes = [_vp, C.c_float, C.c_float, _vp, _vp, C.c_int64, _vp]
+lib.rl_scale_by_inverse_count.restype = C.c_int
+lib.rl_scale_by_inverse_count.argtypes = [_vp, C.c_int64, _vp, _vp]
 lib.rl_status_string.restype = C.c_char_p
 lib.rl_status_string.argtypes = [C.c_int]
 lib.rl_build_info.restype = C.c_char_p
@@ -95,7 +99,8 @@ lib.rl_trace_durations.argtypes = [_vp, C.c_int32]
 EXPORTED = ["rl_workspace_size", "rl_batch_prepare", "rl_logprob_fwd", "rl_grpo_group_stats",
             "rl_grpo_advantage", "rl_policy_loss_fwd_bwd", "rl_status_string", "rl_build_info",
             "rl_launch_count", "rl_trace_begin", "rl_trace_end", "rl_trace_durations",
-            "rl_logprob_partials", "rl_logprob_merge", "rl_policy_loss_fwd_bwd_vp"]
+            "rl_logprob_partials", "rl_logprob_merge", "rl_policy_loss_fwd_bwd_vp",
+            "rl_minibatch_early_stop", "rl_scale_by_inverse_count"]
 
 
 class RLHeadError(RuntimeError):
@@ -295,6 +300,21 @@ def rl_policy_loss_fwd_bwd_vp(head: Head, hidden, weight, batch: Batch, parts_al
                                          _ptr(grad_hidden), _ptr(grad_weight), _ptr(stats),
                                          _ptr(buf), buf.numel(), _stream(stream)),
            "rl_policy_loss_fwd_bwd_vp")
+
+
+def rl_minibatch_early_stop(stats, stop_flag, grad_weight, max_ratio: float = 0.0,
+                            max_mean_ratio: float = 0.0, stream=None):
+    """device-side decision into stop_flag (int32[1]); zeroes grad_weight if set."""
+    n = 0 if grad_weight is None else int(grad_weight.numel())
+    _check(lib.rl_minibatch_early_stop(_ptr(stats), float(max_ratio), float(max_mean_ratio),
+                                       _ptr(stop_flag), _ptr(grad_weight), n, _stream(stream)),
+           "rl_minibatch_early_stop")
+
+
+def rl_scale_by_inverse_count(x, count, stream=None):
+    """x *= 1/count (device int64[1]); deferred normalisation of streaming mode."""
+    _check(lib.rl_scale_by_inverse_count(_ptr(x), int(x.numel()), _ptr(count), _stream(stream)),
+           "rl_scale_by_inverse_count")
 
 
 def rl_launch_count() -> int:

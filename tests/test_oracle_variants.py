@@ -130,3 +130,31 @@ def test_entropy_bonus_uniform_has_no_gradient():
                                    oracle.LossParams(entropy_coef=0.3))
     np.testing.assert_allclose(a["dH"], b["dH"], atol=1e-15)
     assert b["loss"] == pytest.approx(a["loss"] - 0.3 * math.log(V), abs=1e-14)
+
+
+def test_streaming_deferred_scale_equals_token_mean():
+    """P:L433-436 elastic pipelining: micro-batches with loss_scale = 1 then
+    x 1/N at the end == the token mean computed with N known upfront."""
+    H, W, y, cu, mask, adv = _problem(seed=9)
+    lp = oracle.logprob_fwd(H, W, cu, mask, y)["logp"]
+    old = lp + 0.03
+    N = int(mask.sum())
+    whole = oracle.policy_loss_fwd_bwd(H, W, cu, mask, y, old, adv)
+    acc = np.zeros_like(whole["dW"])
+    for s0, s1 in [(0, 2), (2, 3)]:
+        r0, r1 = cu[s0], cu[s1]
+        part = oracle.policy_loss_fwd_bwd(H[r0:r1], W, cu[s0:s1 + 1] - r0, mask[r0:r1], y[r0:r1],
+                                          old[r0:r1], adv[s0:s1], oracle.LossParams(loss_scale=1.0))
+        acc += part["dW"]
+    np.testing.assert_allclose(oracle.head.scale_by_inverse_count(acc, N), whole["dW"], atol=1e-16)
+    assert (oracle.head.scale_by_inverse_count(acc, 0) == 0).all()
+
+
+def test_minibatch_early_stop_rule():
+    """discard on too large importance ratio (max or token mean)."""
+    st = dict(ratio_max=3.5, ratio_sum=120.0, tokens=100)
+    es = oracle.head.minibatch_early_stop
+    assert es(st, max_ratio=3.0) and not es(st, max_ratio=4.0)
+    assert es(st, max_mean_ratio=1.1) and not es(st, max_mean_ratio=1.25)
+    assert not es(st) and not es(dict(st, tokens=0), max_mean_ratio=1.0)
+    assert not es(st, max_ratio=3.5)                 # strictly larger discards

@@ -189,3 +189,63 @@ class PolicyLossStep:
         all_reduce_(self.grad_w, "sum", self.group)
         reduce_stats_(self.stats, self.group)
         return self.stats
+
+
+class StreamingPolicyLoss:
+    """Micro-batch streaming interface (NEXT-2; P:L433-436 elastic pipelining:
+    "output data can be forwarded once a configured size of data batch is
+    ready ... the micro-batch defines forward/backward units, while the
+    global-batch determines when model updates occur").
+
+    Micro-batches are fed as they arrive (e.g. from a data channel), before the
+    global batch -- and so N -- is known: each runs at once with loss_scale = 1
+    while its token count accumulates on the device. ``finish()`` all-reduces
+    N, applies the deferred 1/N to dW (the caller applies the same factor to
+    the trunk gradients it accumulated from each micro-batch's dL/dH),
+    all-reduces dW and the stats, and evaluates the minibatch early stop
+    ("discard minibatches with too large importance ratio") on the
+    device: ``stop_flag`` = 1 and dW = 0 when the update is discarded.
+    """
+
+    def __init__(self, head, weight, params=None, group=None, max_ratio: float = 0.0,
+                 max_mean_ratio: float = 0.0):
+        import torch
+        from . import rlhead as R
+        self.R = R
+        self.head, self.W, self.group = head, weight, group
+        self.params = params or R.LossParams()
+        self.params.loss_scale = 1.0
+        self.params.n_tokens_global = None
+        if self.params.seq_mean:
+            raise ValueError("streaming mode defers 1/N: token-mean aggregation only")
+        dev = weight.device
+        self.max_ratio, self.max_mean_ratio = max_ratio, max_mean_ratio
+        self.n_tokens = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.stop_flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.grad_w = torch.zeros(weight.shape[0], weight.shape[1], dtype=torch.float32, device=dev)
+        self.stats = R.new_stats(dev)
+        self.ws = R.Workspace(dev)
+        self.ws_prep = R.Workspace(dev)
+
+    def begin(self):
+        self.n_tokens.zero_()
+        self.stop_flag.zero_()
+        self.grad_w.zero_()
+        self.stats.zero_()
+
+    def feed(self, hidden, batch, old_logp, adv, logp, grad_hidden, entropy=None):
+        R = self.R
+        R.rl_batch_prepare(self.head, batch, n_accum=self.n_tokens, ws=self.ws_prep)
+        R.rl_policy_loss_fwd_bwd(self.head, hidden, self.W, batch, old_logp, adv, self.params,
+                                 logp, grad_hidden, self.grad_w, entropy=entropy,
+                                 stats=self.stats, ws=self.ws)
+
+    def finish(self):
+        R = self.R
+        all_reduce_(self.n_tokens, "sum", self.group)
+        R.rl_scale_by_inverse_count(self.grad_w, self.n_tokens)
+        all_reduce_(self.grad_w, "sum", self.group)
+        reduce_stats_(self.stats, self.group)
+        R.rl_minibatch_early_stop(self.stats, self.stop_flag, self.grad_w, self.max_ratio,
+                                  self.max_mean_ratio)
+        return self.stats

@@ -294,7 +294,8 @@ def _kl_k3(logp, ref, c):
 
 def policy_loss_fwd_bwd(hidden, weight, cu_seqlens, mask, targets, old_logp, adv_seq,
                         params: LossParams | None = None, n_global=None,
-                        inv_temperature=1.0, want_grads=True, ref_logp=None, n_seqs_global=None):
+                        inv_temperature=1.0, want_grads=True, ref_logp=None, n_seqs_global=None,
+                        adv_per_token=False):
     """Forward + backward of the masked clipped-ratio loss (token mean by default).
 
     hidden [R, h]; weight [V, h]; old_logp [R]; adv_seq [S] (one advantage per
@@ -353,7 +354,8 @@ def policy_loss_fwd_bwd(hidden, weight, cu_seqlens, mask, targets, old_logp, adv
         gc = np.zeros(len(idx))
         gec = np.zeros(len(idx))
         for j, t in enumerate(idx):
-            A = float(adv[bk["row_seq"][t]])
+            # GRPO: one advantage per sequence; PPO/GAE (NEXT-4): one per token
+            A = float(adv[t] if adv_per_token else adv[bk["row_seq"][t]])
             r, loss, dldlp, clo, chi = _surrogate(float(lp[j]), float(old[t]), A, p)
             k, dk = (0.0, 0.0) if ref is None else _kl_k3(float(lp[j]), float(ref[t]),
                                                             p.logratio_clamp)

@@ -162,6 +162,8 @@ typedef struct {
   int32_t seq_mean;               /* 0 token mean, 1 seq-mean-token-mean             */
   const float *ref_logp;          /* [R] device: reference-policy log-probs          */
   const int64_t *n_seqs_global;   /* device: S (seq_mean); see rl_batch_prepare      */
+  int32_t adv_per_token;          /* 0: adv is [S] per sequence (GRPO); 1: adv is [R]
+                                     per row (PPO/GAE, NEXT-4)                        */
 } rl_loss_params;
 
 /* Loss statistics, device resident, ACCUMULATED (+=) by every call. The
@@ -213,6 +215,39 @@ RL_API rl_status rl_minibatch_early_stop(const rl_loss_stats *stats, float max_r
                                          float *grad_weight, int64_t n, rl_stream_t stream);
 RL_API rl_status rl_scale_by_inverse_count(float *x, int64_t n, const int64_t *count,
                                            rl_stream_t stream);
+
+/* ---- PPO pieces (NEXT-4; DESIGN.md §3 #30-#32) --------------------------
+ * rl_gae: generalised advantage estimation over packed trajectories
+ * (embodied PPO; the RLHF critic). Trajectory s owns steps
+ * [cu_steps[s], cu_steps[s+1]); per step t: rewards, values, dones (uint8,
+ * may be NULL = none); bootstrap[s] (may be NULL = 0) is V after the last step.
+ *   delta_t = r_t + gamma (1-done_t) V_{t+1} - V_t
+ *   A_t = delta_t + gamma lam (1-done_t) A_{t+1};  returns_t = A_t + V_t.
+ * fp64 recurrence, fp32 outputs. */
+RL_API rl_status rl_gae(const float *rewards, const float *values, const uint8_t *dones,
+                        const float *bootstrap, const int32_t *cu_steps, int32_t num_traj,
+                        float gamma, float lam, float *adv, float *returns, rl_stream_t stream);
+
+/* Value head v_t = <w_v, h_t> + b_v on the rows with mask != 0 and the PPO
+ * clipped value loss L_v = scale * sum_t 0.5 max((v-R)^2, (clip(v, v_old-eps,
+ * v_old+eps)-R)^2), scale = 1/N (n_tokens_global) or loss_scale.
+ *   values [R] out (0 on other rows); grad_hidden [R, ld] ACCUMULATED (+=,
+ *   add the value head's dL/dh to the policy's); grad_w [h] fp32 and grad_b
+ *   [1] fp32 (may be NULL) ACCUMULATED; stats (may be NULL) accumulate
+ *   loss_sum, objective, clip_hi_count (= clipped-branch tokens), tokens.
+ * hidden and w_v share hd->dtype; ws from rl_value_workspace_size. */
+typedef struct {
+  float clip_eps;                 /* eps_v >= 0                                     */
+  double loss_scale;              /* used when n_tokens_global is NULL              */
+  const int64_t *n_tokens_global; /* device: N                                       */
+} rl_value_params;
+RL_API size_t rl_value_workspace_size(int32_t hidden, int64_t num_rows);
+RL_API rl_status rl_value_loss_fwd_bwd(const rl_head *hd, const void *hidden, const void *w_v,
+                                       float b_v, const rl_batch *b, const float *returns,
+                                       const float *old_values, const rl_value_params *p,
+                                       float *values, void *grad_hidden, float *grad_w,
+                                       float *grad_b, rl_loss_stats *stats, void *ws,
+                                       size_t ws_bytes, rl_stream_t stream);
 
 /* ---- vocab-parallel head (NEXT-3) ----------------------
  * A vocab shard cannot finish the log-sum-exp alone. Phase 1 on every rank:

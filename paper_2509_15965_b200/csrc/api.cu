@@ -284,8 +284,10 @@ static rl_status loss_impl(const rl_head* hd, const void* hidden, const void* we
       !(p->logratio_clamp > 0.f) || !std::isfinite(p->loss_scale))
     return RL_ERR_INVALID_ARG;
   if (!(p->dual_clip == 0.f || p->dual_clip > 1.f) || !(p->kl_coef >= 0.f) ||
-      !(p->entropy_coef >= 0.f) || (p->seq_mean != 0 && p->seq_mean != 1))
+      !(p->entropy_coef >= 0.f) || (p->seq_mean != 0 && p->seq_mean != 1) ||
+      (p->adv_per_token != 0 && p->adv_per_token != 1))
     return RL_ERR_INVALID_ARG;
+  if (p->adv_per_token && b->num_rows > 0 && !adv) return RL_ERR_INVALID_ARG;
   if (p->kl_coef > 0.f && b->num_rows > 0 && !p->ref_logp) return RL_ERR_INVALID_ARG;
   const bool entropy_on = p->entropy_coef > 0.f;
   WsLayout L;
@@ -334,6 +336,7 @@ static rl_status loss_impl(const rl_head* hd, const void* hidden, const void* we
   a.kl_coef = p->kl_coef;
   a.entropy_coef = p->entropy_coef;
   a.seq_mean = p->seq_mean;
+  a.adv_per_token = p->adv_per_token;
   a.ref_logp = p->kl_coef > 0.f ? p->ref_logp : nullptr;
   a.n_seqs_global = p->n_seqs_global;
   a.cu_seqlens = b->cu_seqlens;

@@ -46,6 +46,7 @@ struct MergeArgs {
   // NEXT-1 variants
   float dual_clip, kl_coef, entropy_coef;
   int32_t seq_mean;
+  int32_t adv_per_token;                // adv indexed by row (PPO) instead of sequence
   const float* ref_logp;                // row space
   const int64_t* n_seqs_global;
   const int32_t* cu_seqlens;            // for n_s (seq_mean)

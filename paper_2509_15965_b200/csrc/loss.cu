@@ -127,7 +127,7 @@ k_merge(MergeArgs a, const WsHeader* __restrict__ hdr, int64_t ldp) {
         const long long N = *a.n_global;
         base = N > 0 ? 1.0 / static_cast<double>(N) : 0.0;
       }
-      const float A = a.adv[sq];
+      const float A = a.adv_per_token ? a.adv[t] : a.adv[sq];
       const float d = lp - a.old_logp[t];
       const float dc = fminf(fmaxf(d, -a.clamp_c), a.clamp_c);
       const float ratio = expf(dc);

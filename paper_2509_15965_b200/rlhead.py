@@ -42,7 +42,13 @@ class rl_loss_params(C.Structure):
     _fields_ = [("clip_lo", C.c_float), ("clip_hi", C.c_float), ("logratio_clamp", C.c_float),
                 ("loss_scale", C.c_double), ("n_tokens_global", C.c_void_p),
                 ("dual_clip", C.c_float), ("kl_coef", C.c_float), ("entropy_coef", C.c_float),
-                ("seq_mean", C.c_int32), ("ref_logp", C.c_void_p), ("n_seqs_global", C.c_void_p)]
+                ("seq_mean", C.c_int32), ("ref_logp", C.c_void_p), ("n_seqs_global", C.c_void_p),
+                ("adv_per_token", C.c_int32)]
+
+
+class rl_value_params(C.Structure):
+    _fields_ = [("clip_eps", C.c_float), ("loss_scale", C.c_double),
+                ("n_tokens_global", C.c_void_p)]
 
 
 class rl_loss_stats(C.Structure):
@@ -85,6 +91,14 @@ lib.rl_minibatch_early_stop.restype = C.c_int
 lib.rl_minibatch_early_stop.argtypes = [_vp, C.c_float, C.c_float, _vp, _vp, C.c_int64, _vp]
 lib.rl_scale_by_inverse_count.restype = C.c_int
 lib.rl_scale_by_inverse_count.argtypes = [_vp, C.c_int64, _vp, _vp]
+lib.rl_gae.restype = C.c_int
+lib.rl_gae.argtypes = [_vp, _vp, _vp, _vp, _vp, C.c_int32, C.c_float, C.c_float, _vp, _vp, _vp]
+lib.rl_value_workspace_size.restype = C.c_size_t
+lib.rl_value_workspace_size.argtypes = [C.c_int32, C.c_int64]
+lib.rl_value_loss_fwd_bwd.restype = C.c_int
+lib.rl_value_loss_fwd_bwd.argtypes = [C.POINTER(rl_head), _vp, _vp, C.c_float, C.POINTER(rl_batch),
+                                      _vp, _vp, C.POINTER(rl_value_params), _vp, _vp, _vp, _vp,
+                                      _vp, _vp, _sz, _vp]
 lib.rl_status_string.restype = C.c_char_p
 lib.rl_status_string.argtypes = [C.c_int]
 lib.rl_build_info.restype = C.c_char_p
@@ -100,7 +114,8 @@ EXPORTED = ["rl_workspace_size", "rl_batch_prepare", "rl_logprob_fwd", "rl_grpo_
             "rl_grpo_advantage", "rl_policy_loss_fwd_bwd", "rl_status_string", "rl_build_info",
             "rl_launch_count", "rl_trace_begin", "rl_trace_end", "rl_trace_durations",
             "rl_logprob_partials", "rl_logprob_merge", "rl_policy_loss_fwd_bwd_vp",
-            "rl_minibatch_early_stop", "rl_scale_by_inverse_count"]
+            "rl_minibatch_early_stop", "rl_scale_by_inverse_count", "rl_gae",
+            "rl_value_workspace_size", "rl_value_loss_fwd_bwd"]
 
 
 class RLHeadError(RuntimeError):
@@ -172,12 +187,13 @@ class LossParams:
     seq_mean: bool = False
     ref_logp: object = None         # device fp32 [R] (needed when kl_coef > 0)
     n_seqs_global: object = None    # device int64[1]: S for seq_mean
+    adv_per_token: bool = False     # adv [R] per row (PPO/GAE) instead of [S]
 
     def c(self) -> rl_loss_params:
         return rl_loss_params(self.clip_lo, self.clip_hi, self.logratio_clamp, self.loss_scale,
                               _ptr(self.n_tokens_global), self.dual_clip, self.kl_coef,
                               self.entropy_coef, int(bool(self.seq_mean)), _ptr(self.ref_logp),
-                              _ptr(self.n_seqs_global))
+                              _ptr(self.n_seqs_global), int(bool(self.adv_per_token)))
 
 
 class Workspace:
@@ -315,6 +331,30 @@ def rl_scale_by_inverse_count(x, count, stream=None):
     """x *= 1/count (device int64[1]); deferred normalisation of streaming mode."""
     _check(lib.rl_scale_by_inverse_count(_ptr(x), int(x.numel()), _ptr(count), _stream(stream)),
            "rl_scale_by_inverse_count")
+
+
+def rl_gae(rewards, values, cu_steps, gamma: float, lam: float, adv, returns, dones=None,
+           bootstrap=None, stream=None):
+    """GAE over packed trajectories (NEXT-4)."""
+    _check(lib.rl_gae(_ptr(rewards), _ptr(values), _ptr(dones), _ptr(bootstrap), _ptr(cu_steps),
+                      int(cu_steps.shape[0]) - 1, float(gamma), float(lam), _ptr(adv),
+                      _ptr(returns), _stream(stream)), "rl_gae")
+
+
+def rl_value_loss_fwd_bwd(head: Head, hidden, w_v, b_v: float, batch: Batch, returns, old_values,
+                          values, grad_hidden, grad_w, grad_b=None, clip_eps: float = 0.2,
+                          n_tokens_global=None, loss_scale: float = 1.0, stats=None,
+                          ws: Workspace | None = None, stream=None):
+    """Value head + clipped value loss (NEXT-4); grad_hidden/grad_w/grad_b accumulate."""
+    hd, b = head.c(), batch.c()
+    p = rl_value_params(float(clip_eps), float(loss_scale), _ptr(n_tokens_global))
+    ws = ws or Workspace()
+    buf = ws.get(int(lib.rl_value_workspace_size(hd.hidden, b.num_rows)))
+    _check(lib.rl_value_loss_fwd_bwd(C.byref(hd), _ptr(hidden), _ptr(w_v), float(b_v), C.byref(b),
+                                     _ptr(returns), _ptr(old_values), C.byref(p), _ptr(values),
+                                     _ptr(grad_hidden), _ptr(grad_w), _ptr(grad_b), _ptr(stats),
+                                     _ptr(buf), buf.numel(), _stream(stream)),
+           "rl_value_loss_fwd_bwd")
 
 
 def rl_launch_count() -> int:

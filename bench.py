@@ -31,7 +31,6 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "policy-loss fwd+bwd tokens/s at 1/2/4/8 B200; % bf16 tensor-core peak"
-GEMM_KINDS = ("gemm_lse", "gemm_dz", "gemm_dh", "gemm_dw")
 
 
 def parse():
@@ -261,9 +260,10 @@ def main():
     pk = peaks()
     kinds = tr.by_kind()
     per_kind = {k: {"launches": c, "ms_total": round(t, 3)} for k, (c, t) in kinds.items()}
-    gemm = {k: kinds[k] for k in GEMM_KINDS if k in kinds}
+    units = rl.rlhead.GEMM_FLOP_UNITS        # a fused dH+dW launch does 2 x 2hV per token
+    gemm = {k: kinds[k] for k in units if k in kinds}
     dom = max(gemm, key=lambda k: gemm[k][1])
-    dom_flops = 2.0 * cfg.hidden * cfg.vocab * tokens_local * args.steps
+    dom_flops = units[dom] * 2.0 * cfg.hidden * cfg.vocab * tokens_local * args.steps
     achieved = dom_flops / (gemm[dom][1] / 1e3) / 1e12
     step_tflops_exec = 8.0 * cfg.hidden * cfg.vocab * value / 1e12
     step_tflops_alg = 6.0 * cfg.hidden * cfg.vocab * value / 1e12

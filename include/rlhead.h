@@ -288,7 +288,8 @@ typedef enum {
   RL_K_PREPARE = 0, RL_K_GATHER = 1, RL_K_GEMM_LSE = 2, RL_K_MERGE = 3,
   RL_K_GEMM_DZ = 4, RL_K_GEMM_DH = 5, RL_K_GEMM_DW = 6, RL_K_GRPO = 7,
   RL_K_SIMT_FWD = 8, RL_K_SIMT_BWD = 9, RL_K_REDUCE = 10, RL_K_MISC = 11,
-  RL_K_NUM_KINDS = 12
+  RL_K_GEMM_DHDW = 12, /* fused dH + dW launch (two GEMMs of 2hV flop/token each) */
+  RL_K_NUM_KINDS = 13
 } rl_kernel_kind;
 
 /* Tracing (not thread-safe; for benchmarks, cf. the worker-group timers of

@@ -61,7 +61,9 @@ struct TcCfg {
   static constexpr int ACC_STAGES = NB == 1 ? 2 : 1;
 };
 
-enum { EPI_LSE = 0, EPI_DZ = 1, EPI_ROWS = 2, EPI_ACC = 3 };
+// EPI_BWD: problem 0 = dH (A K-major, EPI_ROWS), problem 1 = dW (A MN-major,
+// EPI_ACC), both with MN-major B, in one persistent launch.
+enum { EPI_LSE = 0, EPI_DZ = 1, EPI_ROWS = 2, EPI_ACC = 3, EPI_BWD = 4 };
 
 struct TcArgs {
   int64_t M, K;        // host values (used unless m_dyn / k_dyn)
@@ -69,6 +71,9 @@ struct TcArgs {
   int32_t n_tiles;
   int32_t m_dyn, k_dyn;
   int32_t group_m;
+  // second problem of EPI_BWD (the dW GEMM)
+  int64_t M2, K2;
+  int32_t n_tiles2, m_dyn2, k_dyn2, group_m2;
   int32_t l2_policy;   // TMA L2 hint: 0 normal, 1 evict_last, 2 evict_first
   const WsHeader* hdr;
   float inv_temp;
@@ -104,6 +109,20 @@ __device__ __forceinline__ void tile_coords(int64_t tile, int64_t m_tiles, int n
   nb = static_cast<int>(local / gm);
 }
 
+// One GEMM problem of a launch: rows, K blocks and its share of the tile space.
+struct Prob {
+  int64_t M = 0, num_k = 0, m_tiles = 0, tiles = 0;
+  int32_t n_tiles = 1, group_m = 1;
+  __device__ void init(int64_t M_, int64_t K_, int tile_m, int32_t n_tiles_, int32_t group_m_) {
+    M = M_;
+    m_tiles = (M_ + tile_m - 1) / tile_m;
+    num_k = (K_ + TC_BK - 1) / TC_BK;
+    n_tiles = n_tiles_;
+    group_m = group_m_;
+    tiles = num_k > 0 ? m_tiles * n_tiles_ : 0;
+  }
+};
+
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<const uint32_t*>(&v);
@@ -112,6 +131,7 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 template <int CG, int NB, int AMN, int BMN, int EPI>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+          const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2,
           const TcArgs args) {
   using C = TcCfg<CG, NB>;
   extern __shared__ uint8_t smem_raw[];
@@ -131,6 +151,10 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
+    if constexpr (EPI == EPI_BWD) {
+      tma_prefetch_desc(&tmA2);
+      tma_prefetch_desc(&tmB2);
+    }
     for (int i = 0; i < C::STAGES; ++i) {
       mbar_init(full + i, CG);     // CG producers arrive (remote for the peer)
       mbar_init(empty + i, 1);     // one (multicast) commit per phase
@@ -151,13 +175,24 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
+  // Tile space: problem 0, then (EPI_BWD only) problem 1 -- the dH and dW
+  // GEMMs of one backward in a single persistent launch, so the short last
+  // wave of one fills with tiles of the other.
   const int64_t T = args.hdr->n_active;
-  const int64_t M = args.m_dyn ? T : args.M;
-  const int64_t K = args.k_dyn ? T : args.K;
-  const int64_t m_tiles = (M + C::TILE_M - 1) / C::TILE_M;
-  const int64_t num_k = (K + TC_BK - 1) / TC_BK;
-  const int64_t num_tiles = num_k > 0 ? m_tiles * args.n_tiles : 0;
+  Prob P0, P1;
+  P0.init(args.m_dyn ? T : args.M, args.k_dyn ? T : args.K, C::TILE_M, args.n_tiles, args.group_m);
+  if constexpr (EPI == EPI_BWD)
+    P1.init(args.m_dyn2 ? T : args.M2, args.k_dyn2 ? T : args.K2, C::TILE_M, args.n_tiles2,
+            args.group_m2);
+  const int64_t num_tiles = P0.tiles + P1.tiles;
   const int64_t cid = blockIdx.x / CG, ncl = gridDim.x / CG;
+  // per tile: which problem, its coordinates and K extent
+  auto locate = [&](int64_t tile, bool& second, int64_t& mb, int& nb) -> const Prob& {
+    second = tile >= P0.tiles;
+    const Prob& P = second ? P1 : P0;
+    tile_coords(second ? tile - P0.tiles : tile, P.m_tiles, P.n_tiles, P.group_m, mb, nb);
+    return P;
+  };
 
   if (warp == 0) {
     if (lane == 0) {
@@ -170,11 +205,15 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       for (int64_t tile = cid; tile < num_tiles; tile += ncl) {
         int64_t mb;
         int nb;
-        tile_coords(tile, m_tiles, args.n_tiles, args.group_m, mb, nb);
+        bool second;
+        const Prob& P = locate(tile, second, mb, nb);
+        const bool amn = EPI == EPI_BWD ? second : (AMN != 0);
+        const CUtensorMap* mA = second ? &tmA2 : &tmA;
+        const CUtensorMap* mB = second ? &tmB2 : &tmB;
         const int32_t m0 = static_cast<int32_t>(mb * C::TILE_M + rank * TC_BM);
         // part p of this CTA's B: global rows n0 + p*256 + [0, PART_ROWS)
         const int32_t n0 = nb * C::TILE_N + static_cast<int32_t>(rank) * C::PART_ROWS;
-        for (int64_t kb = 0; kb < num_k; ++kb) {
+        for (int64_t kb = 0; kb < P.num_k; ++kb) {
           mbar_wait(empty + stage, phase ^ 1);
           if (leader) mbar_arrive_expect_tx(full + stage, C::STAGE_BYTES * CG);
           else mbar_arrive_cluster(full + stage, 0);
@@ -185,11 +224,11 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             if constexpr (CG == 2) tma_load_2d_2sm(m, full + stage, dst, c0, c1, pol);
             else tma_load_2d(m, full + stage, dst, c0, c1, pol);
           };
-          if (AMN) {
-            load(&tmA, a_dst, m0, k0);
-            load(&tmA, a_dst + 8192, m0 + 64, k0);
+          if (amn) {
+            load(mA, a_dst, m0, k0);
+            load(mA, a_dst + 8192, m0 + 64, k0);
           } else {
-            load(&tmA, a_dst, k0, m0);
+            load(mA, a_dst, k0, m0);
           }
 #pragma unroll
           for (int p = 0; p < NB; ++p) {
@@ -197,9 +236,9 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             const int32_t np = n0 + p * TC_BN;
             if (BMN) {
 #pragma unroll
-              for (int i = 0; i < C::PART_ROWS / 64; ++i) load(&tmB, pd + i * 8192, np + 64 * i, k0);
+              for (int i = 0; i < C::PART_ROWS / 64; ++i) load(mB, pd + i * 8192, np + 64 * i, k0);
             } else {
-              load(&tmB, pd, k0, np);
+              load(mB, pd, k0, np);
             }
           }
           if (++stage == C::STAGES) {
@@ -212,24 +251,31 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   } else if (warp == 1) {
     if (lane == 0 && leader) {
       // ------------------------------------------------------- MMA issuer
-      constexpr uint32_t IDESC = umma_idesc_bf16(TC_BM * CG, TC_BN, AMN, BMN);
+      constexpr uint32_t IDESC_K = umma_idesc_bf16(TC_BM * CG, TC_BN, 0, BMN);
+      constexpr uint32_t IDESC_MN = umma_idesc_bf16(TC_BM * CG, TC_BN, 1, BMN);
       const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int64_t tile = cid; tile < num_tiles; tile += ncl) {
+        int64_t mb_unused;
+        int nb_unused;
+        bool second;
+        const Prob& P = locate(tile, second, mb_unused, nb_unused);
+        const bool amn = EPI == EPI_BWD ? second : (AMN != 0);
+        const uint32_t IDESC = amn ? IDESC_MN : IDESC_K;
         mbar_wait(tempty + acc, acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * TC_BN);
-        for (int64_t kb = 0; kb < num_k; ++kb) {
+        for (int64_t kb = 0; kb < P.num_k; ++kb) {
           mbar_wait(full + stage, phase);
           tc_fence_after();
           const uint32_t a_addr = a_base + stage * C::A_BYTES;
           const uint32_t b_addr = b_base + stage * C::B_BYTES;
 #pragma unroll
           for (int k = 0; k < TC_BK / 16; ++k) {
-            const uint64_t ad = AMN ? umma_desc_sw128(a_addr + k * 2048, 8192, 1024)
+            const uint64_t ad = amn ? umma_desc_sw128(a_addr + k * 2048, 8192, 1024)
                                     : umma_desc_sw128(a_addr + k * 32, 0, 1024);
             const uint32_t accum = (kb > 0 || k > 0) ? 1u : 0u;
 #pragma unroll
@@ -271,11 +317,13 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     for (int64_t tile = cid; tile < num_tiles; tile += ncl) {
       int64_t mb;
       int nb;
-      tile_coords(tile, m_tiles, args.n_tiles, args.group_m, mb, nb);
+      bool second;
+      const Prob& P = locate(tile, second, mb, nb);
       const int64_t row = mb * C::TILE_M + rank * TC_BM + rit;
       const int n0 = nb * C::TILE_N;
-      const bool row_ok = row < M;
-      static_assert(NB == 1 || EPI == EPI_ROWS || EPI == EPI_ACC, "512-wide tiles: dH/dW only");
+      const bool row_ok = row < P.M;
+      static_assert(NB == 1 || EPI == EPI_ROWS || EPI == EPI_ACC || EPI == EPI_BWD,
+                    "512-wide tiles: dH/dW only");
       mbar_wait(tfull + acc, acc_phase);
       tc_fence_after();
       const uint32_t taddr =
@@ -384,7 +432,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                               make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]),
                               st_pol);
         }
-      } else if constexpr (EPI == EPI_ROWS) {
+      } else if (EPI == EPI_ROWS || (EPI == EPI_BWD && !second)) {
         const int64_t orow = row_ok ? static_cast<int64_t>(args.row_idx[row]) : 0;
         uint4* dst = reinterpret_cast<uint4*>(args.out + orow * args.ld_out + n0);
 #pragma unroll 1
@@ -403,7 +451,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
               dst[c * 4 + q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
           }
         }
-      } else {  // EPI_ACC
+      } else {  // EPI_ACC (or the dW half of EPI_BWD)
         float4* dst = reinterpret_cast<float4*>(args.acc + row * args.ld_acc + n0);
 #pragma unroll 1
         for (int c = 0; c < C::TILE_N / 32; ++c) {
@@ -508,8 +556,9 @@ int tc_cta_group() {
 }
 
 template <int CG, int NB, int AMN, int BMN, int EPI>
-static rl_status run_gemm(const CUtensorMap& a, const CUtensorMap& b, const TcArgs& args,
-                          int64_t m_extent, int kind, cudaStream_t s) {
+static rl_status run_gemm(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& a2,
+                          const CUtensorMap& b2, const TcArgs& args, int64_t tiles_bound,
+                          int kind, cudaStream_t s) {
   using C = TcCfg<CG, NB>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
@@ -518,7 +567,6 @@ static rl_status run_gemm(const CUtensorMap& a, const CUtensorMap& b, const TcAr
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
   });
   if (attr_err != cudaSuccess) return RL_ERR_CUDA;
-  const int64_t tiles_bound = ceil_div(m_extent, C::TILE_M) * args.n_tiles;
   if (tiles_bound <= 0) return RL_OK;
   const int64_t clusters_max = num_sms() / CG;
   const int64_t clusters = tiles_bound < clusters_max ? tiles_bound : clusters_max;
@@ -535,7 +583,8 @@ static rl_status run_gemm(const CUtensorMap& a, const CUtensorMap& b, const TcAr
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   TraceScope ts(kind, s);
-  if (cudaLaunchKernelEx(&cfg, k_tc_gemm<CG, NB, AMN, BMN, EPI>, a, b, args) != cudaSuccess)
+  if (cudaLaunchKernelEx(&cfg, k_tc_gemm<CG, NB, AMN, BMN, EPI>, a, b, a2, b2, args) !=
+      cudaSuccess)
     return RL_ERR_CUDA;
   RLH_CHECK_LAUNCH();
   return RL_OK;
@@ -548,13 +597,16 @@ static rl_status run_narrow(const CUtensorMap& a, const CUtensorMap& b, TcArgs t
   t.n_tiles = static_cast<int32_t>(ceil_div(t.N, TC_BN));
   t.group_m = env_int("RLHEAD_GROUP_M", 32) / tc_cta_group();
   if (t.group_m < 1) t.group_m = 1;
-  if (tc_cta_group() == 2) return run_gemm<2, 1, AMN, BMN, EPI>(a, b, t, m_extent, kind, s);
-  return run_gemm<1, 1, AMN, BMN, EPI>(a, b, t, m_extent, kind, s);
+  const int cg = tc_cta_group();
+  const int64_t tiles = ceil_div(m_extent, TC_BM * cg) * t.n_tiles;
+  if (cg == 2) return run_gemm<2, 1, AMN, BMN, EPI>(a, b, a, b, t, tiles, kind, s);
+  return run_gemm<1, 1, AMN, BMN, EPI>(a, b, a, b, t, tiles, kind, s);
 }
 
 // Long-K dH/dW GEMMs: 256 x 512 pair tiles (all 512 TMEM columns), rastered
 // N-fastest so the CTA pairs sharing an A panel run together.
 static bool wide_bwd() { return tc_cta_group() == 2 && env_int("RLHEAD_WIDE", 1) != 0; }
+static bool fused_bwd() { return wide_bwd() && env_int("RLHEAD_FUSED_BWD", 1) != 0; }
 template <int AMN, int BMN, int EPI>
 static rl_status run_wide(const CUtensorMap& a, const CUtensorMap& b, TcArgs t, int64_t m_extent,
                           int kind, cudaStream_t s) {
@@ -562,11 +614,14 @@ static rl_status run_wide(const CUtensorMap& a, const CUtensorMap& b, TcArgs t, 
   if (t.group_m < 1) t.group_m = 1;
   if (wide_bwd()) {
     t.n_tiles = static_cast<int32_t>(ceil_div(t.N, 2 * TC_BN));
-    return run_gemm<2, 2, AMN, BMN, EPI>(a, b, t, m_extent, kind, s);
+    return run_gemm<2, 2, AMN, BMN, EPI>(a, b, a, b, t, ceil_div(m_extent, 2 * TC_BM) * t.n_tiles,
+                                         kind, s);
   }
   t.n_tiles = static_cast<int32_t>(ceil_div(t.N, TC_BN));
-  if (tc_cta_group() == 2) return run_gemm<2, 1, AMN, BMN, EPI>(a, b, t, m_extent, kind, s);
-  return run_gemm<1, 1, AMN, BMN, EPI>(a, b, t, m_extent, kind, s);
+  const int cg = tc_cta_group();
+  const int64_t tiles = ceil_div(m_extent, TC_BM * cg) * t.n_tiles;
+  if (cg == 2) return run_gemm<2, 1, AMN, BMN, EPI>(a, b, a, b, t, tiles, kind, s);
+  return run_gemm<1, 1, AMN, BMN, EPI>(a, b, a, b, t, tiles, kind, s);
 }
 
 static TcArgs base_args(const rl_head* hd, const WsLayout& L, char* ws) {
@@ -631,39 +686,46 @@ rl_status launch_tc_bwd(const rl_head* hd, const void* weight, void* grad_hidden
     if (st != RL_OK) return st;
   }
   // N6: dH[T, h] = dZ[T, V] W[V, h]; rows -> grad_hidden[active_idx[r]].
-  {
-    CUtensorMap ma, mb;
-    if (!make_map(&ma, dz, V, L.Rp, static_cast<uint64_t>(L.Vp) * 2, TC_BM) ||
-        !make_map(&mb, weight, h, V, static_cast<uint64_t>(h) * 2, 64))
-      return RL_ERR_CUDA;
-    TcArgs t = base_args(hd, L, ws);
-    t.M = L.Rp;
-    t.m_dyn = 1;
-    t.K = V;
-    t.N = h;
-    t.out = static_cast<__nv_bfloat16*>(grad_hidden);
-    t.ld_out = hd->ld_hidden;
-    t.row_idx = reinterpret_cast<const int32_t*>(ws + L.off_active);
-    st = run_wide<0, 1, EPI_ROWS>(ma, mb, t, L.Rp, RL_K_GEMM_DH, s);
-    if (st != RL_OK) return st;
-  }
   // N7: dW[V, h] += dZ^T[V, T] Hc[T, h].
-  {
-    CUtensorMap ma, mb;
-    if (!make_map(&ma, dz, V, L.Rp, static_cast<uint64_t>(L.Vp) * 2, 64) ||
-        !make_map(&mb, ws + L.off_hc, h, L.Rp, static_cast<uint64_t>(h) * 2, 64))
-      return RL_ERR_CUDA;
-    TcArgs t = base_args(hd, L, ws);
-    t.M = V;
-    t.K = L.Rp;
-    t.k_dyn = 1;
-    t.N = h;
+  CUtensorMap ma6, mb6, ma7, mb7;
+  if (!make_map(&ma6, dz, V, L.Rp, static_cast<uint64_t>(L.Vp) * 2, TC_BM) ||
+      !make_map(&mb6, weight, h, V, static_cast<uint64_t>(h) * 2, 64) ||
+      !make_map(&ma7, dz, V, L.Rp, static_cast<uint64_t>(L.Vp) * 2, 64) ||
+      !make_map(&mb7, ws + L.off_hc, h, L.Rp, static_cast<uint64_t>(h) * 2, 64))
+    return RL_ERR_CUDA;
+  TcArgs t6 = base_args(hd, L, ws);
+  t6.M = L.Rp;
+  t6.m_dyn = 1;
+  t6.K = V;
+  t6.N = h;
+  t6.out = static_cast<__nv_bfloat16*>(grad_hidden);
+  t6.ld_out = hd->ld_hidden;
+  t6.row_idx = reinterpret_cast<const int32_t*>(ws + L.off_active);
+  TcArgs t7 = base_args(hd, L, ws);
+  t7.M = V;
+  t7.K = L.Rp;
+  t7.k_dyn = 1;
+  t7.N = h;
+  t7.acc = grad_weight;
+  t7.ld_acc = h;
+  if (fused_bwd()) {
+    // one persistent launch over the dH tiles then the dW tiles: the last
+    // (partial) wave of dH fills with dW tiles instead of idling.
+    TcArgs t = t6;
+    t.n_tiles = static_cast<int32_t>(ceil_div(h, 2 * TC_BN));
+    t.group_m = std::max(1, env_int("RLHEAD_GROUP_M_BWD", 1));
+    t.M2 = V;
+    t.K2 = L.Rp;
+    t.k_dyn2 = 1;
+    t.n_tiles2 = t.n_tiles;
+    t.group_m2 = t.group_m;
     t.acc = grad_weight;
     t.ld_acc = h;
-    st = run_wide<1, 1, EPI_ACC>(ma, mb, t, V, RL_K_GEMM_DW, s);
-    if (st != RL_OK) return st;
+    const int64_t tiles = (ceil_div(L.Rp, 2 * TC_BM) + ceil_div(V, 2 * TC_BM)) * t.n_tiles;
+    return run_gemm<2, 2, 0, 1, EPI_BWD>(ma6, mb6, ma7, mb7, t, tiles, RL_K_GEMM_DHDW, s);
   }
-  return RL_OK;
+  if ((st = run_wide<0, 1, EPI_ROWS>(ma6, mb6, t6, L.Rp, RL_K_GEMM_DH, s)) != RL_OK) return st;
+  return run_wide<1, 1, EPI_ACC>(ma7, mb7, t7, V, RL_K_GEMM_DW, s);
 }
 
 }  // namespace rlh

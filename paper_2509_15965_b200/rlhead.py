@@ -24,7 +24,9 @@ RL_OK, RL_ERR_INVALID_ARG, RL_ERR_UNSUPPORTED, RL_ERR_WORKSPACE, RL_ERR_CUDA = r
 RL_F32, RL_BF16 = 0, 1
 RL_DEVERR_CU_SEQLENS, RL_DEVERR_TARGET, RL_DEVERR_GROUP = 1, 2, 4
 KERNEL_KINDS = ["prepare", "gather", "gemm_lse", "merge", "gemm_dz", "gemm_dh", "gemm_dw",
-                "grpo", "simt_fwd", "simt_bwd", "reduce", "misc"]
+                "grpo", "simt_fwd", "simt_bwd", "reduce", "misc", "gemm_dhdw"]
+# tensor flops per token of each GEMM kind, in units of 2 h V
+GEMM_FLOP_UNITS = {"gemm_lse": 1, "gemm_dz": 1, "gemm_dh": 1, "gemm_dw": 1, "gemm_dhdw": 2}
 
 
 class rl_batch(C.Structure):

@@ -98,7 +98,9 @@ def main():
         ms = t / c
         entry = {"ms": round(ms, 3)}
         if k.startswith("gemm"):
-            entry["tflops"] = round(2.0 * cfg.hidden * cfg.vocab * tok / (ms / 1e3) / 1e12, 1)
+            units = rl.rlhead.GEMM_FLOP_UNITS.get(k, 1)
+            entry["tflops"] = round(units * 2.0 * cfg.hidden * cfg.vocab * tok / (ms / 1e3) / 1e12,
+                                    1)
         out[k] = entry
     print(json.dumps(out))
 

@@ -606,7 +606,10 @@ static rl_status run_narrow(const CUtensorMap& a, const CUtensorMap& b, TcArgs t
 // Long-K dH/dW GEMMs: 256 x 512 pair tiles (all 512 TMEM columns), rastered
 // N-fastest so the CTA pairs sharing an A panel run together.
 static bool wide_bwd() { return tc_cta_group() == 2 && env_int("RLHEAD_WIDE", 1) != 0; }
-static bool fused_bwd() { return wide_bwd() && env_int("RLHEAD_FUSED_BWD", 1) != 0; }
+// Off by default: in same-box A/B runs of bench.py the fused launch drew more
+// power (dH and dW tiles compete for L2 at the transition), lowering clocks
+// for the whole step (-2.3% tokens/s, profiles/r1/SUMMARY.md).
+static bool fused_bwd() { return wide_bwd() && env_int("RLHEAD_FUSED_BWD", 0) != 0; }
 template <int AMN, int BMN, int EPI>
 static rl_status run_wide(const CUtensorMap& a, const CUtensorMap& b, TcArgs t, int64_t m_extent,
                           int kind, cudaStream_t s) {

@@ -14,10 +14,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 @pytest.mark.parametrize("env", [{"RLHEAD_CTA_GROUP": "1"},
                                  {"RLHEAD_CTA_GROUP": "2", "RLHEAD_WIDE": "0"},
                                  {"RLHEAD_CTA_GROUP": "2", "RLHEAD_WIDE": "1",
-                                  "RLHEAD_FUSED_BWD": "0"},
+                                  "RLHEAD_FUSED_BWD": "1"},
                                  {"RLHEAD_CTA_GROUP": "2", "RLHEAD_WIDE": "1",
                                   "RLHEAD_GROUP_M": "16", "RLHEAD_GROUP_M_BWD": "4"}],
-                         ids=["cta1", "cta2-narrow", "cta2-wide-unfused", "cta2-fused-raster"])
+                         ids=["cta1", "cta2-narrow", "cta2-wide-fused", "cta2-unfused-raster"])
 def test_variant_parity(env):
     import torch
     if not torch.cuda.is_available():

@@ -261,7 +261,19 @@ RL_API rl_status rl_value_loss_fwd_bwd(const rl_head *hd, const void *hidden, co
  *     over all shards; grad_hidden is this shard's PARTIAL dL/dH (the caller
  *     all-reduces SUM over the TP group), grad_weight this shard's rows of
  *     dL/dW (accumulated). logp/entropy/stats are identical on every rank of
- *     the TP group (do not sum stats over TP ranks). */
+ *     the TP group (do not sum stats over TP ranks). grad_hidden_fp32:
+ *     0: grad_hidden in hd->dtype with row stride hd->ld_hidden (above);
+ *     1: grad_hidden is float [num_rows][hidden] (row stride = hidden) -- the
+ *        partial dL/dH in fp32, e.g. straight into a symmetric NVLink buffer
+ *        for rl_allreduce_sum_f32; bf16 heads need the tensor-core path, fp32
+ *        heads ld_hidden == hidden;
+ *     2: as 1, but grad_hidden is the NVLS MULTICAST address of a symmetric
+ *        fp32 buffer that the caller zeroed on every rank (then barriered):
+ *        the dL/dH GEMM epilogue adds each tile into every rank's copy through
+ *        the switch (multimem.red.add), so after the call on all ranks (and a
+ *        barrier) every copy holds the TP sum -- the all-reduce fused into the
+ *        GEMM. bf16 tensor-core path only.
+ *     Other values / unsupported combinations: RL_ERR_INVALID_ARG. */
 RL_API rl_status rl_logprob_partials(const rl_head *hd, const void *hidden, const void *weight,
                                      const rl_batch *b, float *parts, void *ws, size_t ws_bytes,
                                      rl_stream_t stream);
@@ -273,9 +285,34 @@ RL_API rl_status rl_policy_loss_fwd_bwd_vp(const rl_head *hd, const void *hidden
                                            const float *parts_all, int32_t nparts,
                                            const float *old_logp, const float *adv,
                                            const rl_loss_params *p, float *logp, float *entropy,
-                                           void *grad_hidden, float *grad_weight,
-                                           rl_loss_stats *stats, void *ws, size_t ws_bytes,
-                                           rl_stream_t stream);
+                                           void *grad_hidden, int32_t grad_hidden_fp32,
+                                           float *grad_weight, rl_loss_stats *stats, void *ws,
+                                           size_t ws_bytes, rl_stream_t stream);
+
+/* ---- sum over NVLink peer memory ----------------------
+ * The exchange step after a GEMM on the sharded path -- the vocab-parallel
+ * SUM of the partial dL/dH (H7 summed over vocab shards: dL/dH = sum_p dZ_p
+ * W_p) -- done by one kernel over a symmetric buffer that every rank of the
+ * group has mapped, no NCCL. buf holds n floats on each rank; on return
+ * (after the caller's next cross-rank barrier) every rank's buf holds the
+ * element-wise sum over the `world` ranks.
+ *   mc_ptr != NULL: the NVLS multicast address of buf (NVSwitch SHARP):
+ *     rank r sums slice r through the switch (multimem.ld_reduce.add) and
+ *     multicasts it back (multimem.st); peer_ptrs is ignored. Rounding order
+ *     is the switch's.
+ *   mc_ptr == NULL: peer_ptrs[q] (a HOST array of `world` device pointers,
+ *     peer_ptrs[rank] = the local buf) are the P2P mappings; rank r loads
+ *     slice r from every peer in rank order 0..world-1 (deterministic) and
+ *     stores the sum to every peer.
+ * The caller brackets the call with cross-rank barriers (all partials written
+ * before; all slices stored after). n % 4 == 0, pointers 16-B aligned,
+ * 1 <= world <= 8, else RL_ERR_INVALID_ARG; world == 1 is a no-op. */
+RL_API rl_status rl_allreduce_sum_f32(float *const *peer_ptrs, float *mc_ptr, int32_t rank,
+                                      int32_t world, int64_t n, rl_stream_t stream);
+/* dst[t][0:hidden] (bf16, row stride ld) = round-to-nearest(src[t][0:hidden])
+ * (fp32, row stride hidden), t < num_rows; hidden even, ld >= hidden even. */
+RL_API rl_status rl_cast_rows_bf16(const float *src, int64_t num_rows, int32_t hidden, void *dst,
+                                   int64_t ld, rl_stream_t stream);
 
 /* ---- introspection / tracing (P:L682-690 worker timers, device-side) ---- */
 RL_API const char *rl_status_string(rl_status s);

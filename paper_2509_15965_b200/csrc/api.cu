@@ -274,7 +274,9 @@ static rl_status loss_impl(const rl_head* hd, const void* hidden, const void* we
                            const rl_batch* b, const float* parts_all, int32_t nparts,
                            const float* old_logp, const float* adv, const rl_loss_params* p,
                            float* logp, float* entropy, void* grad_hidden, float* grad_weight,
-                           rl_loss_stats* stats, void* ws, size_t ws_bytes, rl_stream_t stream) {
+                           rl_loss_stats* stats, void* ws, size_t ws_bytes, rl_stream_t stream,
+                           int gh_mode = 0) {
+  const bool gh_f32 = gh_mode != 0, gh_mc = gh_mode == 2;
   if (!head_ok(hd) || !batch_ok(b) || !weight || !p || !logp || !grad_weight)
     return RL_ERR_INVALID_ARG;
   if (parts_all && nparts < 1) return RL_ERR_INVALID_ARG;
@@ -295,6 +297,11 @@ static rl_status loss_impl(const rl_head* hd, const void* hidden, const void* we
   if (!ws || ws_bytes < L.total) return RL_ERR_WORKSPACE;
   if (!aligned(ws, 256)) return RL_ERR_INVALID_ARG;
   const bool tc = use_tc(hd);
+  // fp32 dL/dH rows [R, hidden]: native for fp32 heads (ld must be hidden),
+  // the tensor-core path's EPI_ROWS fp32 store for bf16 heads.
+  if (gh_f32 && (hd->dtype == RL_BF16 ? !tc : hd->ld_hidden != hd->hidden))
+    return RL_ERR_INVALID_ARG;
+  if (gh_mc && !tc) return RL_ERR_INVALID_ARG;
   if (tc && (!aligned(hidden, 16) || !aligned(weight, 16) || !aligned(grad_hidden, 16) ||
              !aligned(grad_weight, 16)))
     return RL_ERR_INVALID_ARG;
@@ -303,7 +310,9 @@ static rl_status loss_impl(const rl_head* hd, const void* hidden, const void* we
   rl_status st = launch_prepare(hd, b, L, w, nullptr, nullptr, nullptr, nullptr, nullptr, logp,
                                 entropy, nullptr, s);
   if (st != RL_OK) return st;
-  if ((st = launch_zero_inactive(hd, grad_hidden, L, w, s)) != RL_OK) return st;
+  // multicast mode: the caller pre-zeroed every copy; plain stores to a
+  // multicast address are not allowed, and inactive rows receive no adds.
+  if (!gh_mc && (st = launch_zero_inactive(hd, grad_hidden, L, w, s, gh_f32)) != RL_OK) return st;
   if (tc && (st = launch_gather_bf16(hd, hidden, L, w, s)) != RL_OK) return st;
   MergeArgs a{};
   if (parts_all) {
@@ -349,7 +358,10 @@ static rl_status loss_impl(const rl_head* hd, const void* hidden, const void* we
   a.st_i = reinterpret_cast<long long*>(w + L.off_st_i);
   if ((st = launch_merge(L, w, a, s)) != RL_OK) return st;
   if ((st = launch_stats_reduce(L, w, stats, s)) != RL_OK) return st;
-  if (tc) return launch_tc_bwd(hd, weight, grad_hidden, grad_weight, entropy_on, L, w, s);
+  if (tc)
+    return launch_tc_bwd(hd, weight, gh_f32 ? nullptr : grad_hidden,
+                         gh_f32 ? static_cast<float*>(grad_hidden) : nullptr, gh_mc,
+                         grad_weight, entropy_on, L, w, s);
   return launch_simt_bwd(hd, hidden, weight, grad_hidden, grad_weight, entropy_on, L, w, s);
 }
 
@@ -368,12 +380,13 @@ rl_status rl_policy_loss_fwd_bwd_vp(const rl_head* hd, const void* hidden, const
                                     const rl_batch* b, const float* parts_all, int32_t nparts,
                                     const float* old_logp, const float* adv,
                                     const rl_loss_params* p, float* logp, float* entropy,
-                                    void* grad_hidden, float* grad_weight, rl_loss_stats* stats,
-                                    void* ws, size_t ws_bytes, rl_stream_t stream) {
+                                    void* grad_hidden, int32_t grad_hidden_fp32,
+                                    float* grad_weight, rl_loss_stats* stats, void* ws,
+                                    size_t ws_bytes, rl_stream_t stream) {
   if (b && b->num_rows > 0 && !parts_all) return RL_ERR_INVALID_ARG;
-  if (nparts < 1) return RL_ERR_INVALID_ARG;
+  if (nparts < 1 || grad_hidden_fp32 < 0 || grad_hidden_fp32 > 2) return RL_ERR_INVALID_ARG;
   return loss_impl(hd, hidden, weight, b, parts_all, nparts, old_logp, adv, p, logp, entropy,
-                   grad_hidden, grad_weight, stats, ws, ws_bytes, stream);
+                   grad_hidden, grad_weight, stats, ws, ws_bytes, stream, grad_hidden_fp32);
 }
 
 const char* rl_status_string(rl_status s) {

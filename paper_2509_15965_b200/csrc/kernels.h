@@ -17,7 +17,7 @@ rl_status launch_gather_bf16(const rl_head* hd, const void* hidden, const WsLayo
                              cudaStream_t s);
 // grad_hidden rows of inactive rows := 0.
 rl_status launch_zero_inactive(const rl_head* hd, void* grad_hidden, const WsLayout& L, char* ws,
-                               cudaStream_t s);
+                               cudaStream_t s, bool f32_rows = false);
 
 // H2 GRPO.
 rl_status launch_grpo(const float* rewards, const int32_t* gos, int32_t S, int32_t G,
@@ -72,9 +72,12 @@ rl_status launch_simt_bwd(const rl_head* hd, const void* hidden, const void* wei
 // Tensor-core path (bf16, tcgen05/TMEM/TMA).
 rl_status launch_tc_fwd(const rl_head* hd, const void* weight, const WsLayout& L, char* ws,
                         cudaStream_t s);
+// grad_hidden_f32 != NULL: dL/dH as fp32 rows [R, hidden] there instead of
+// bf16 rows into grad_hidden; gh_multicast: grad_hidden_f32 is an NVLS
+// multicast address and the rows are added into every rank's copy.
 rl_status launch_tc_bwd(const rl_head* hd, const void* weight, void* grad_hidden,
-                        float* grad_weight, bool entropy_on, const WsLayout& L, char* ws,
-                        cudaStream_t s);
+                        float* grad_hidden_f32, bool gh_multicast, float* grad_weight,
+                        bool entropy_on, const WsLayout& L, char* ws, cudaStream_t s);
 
 int num_sms();
 

@@ -1,0 +1,121 @@
+// Collectives over NVLink peer memory for the two exchange steps that follow
+// a GEMM on the hot path: the DP sum of dW and the
+// vocab-parallel sum of dL/dH. The GEMM epilogue writes its fp32 result
+// straight into a symmetric buffer (mapped on every rank); after a cross-rank
+// barrier this kernel sums the P copies without NCCL and without staging:
+//  * NVLS (NVLink SHARP, multicast object available): two-shot all-reduce --
+//    rank p pulls its 1/P slice through the switch with
+//    multimem.ld_reduce.add (the switch adds the P copies) and multicasts the
+//    sum back to every rank with multimem.st;
+//  * otherwise P2P: rank p loads its slice from the P peers in rank order
+//    (deterministic), adds, and stores the sum to every peer.
+// A second barrier (caller) makes the result visible before use.
+#include "kernels.h"
+
+namespace rlh {
+
+constexpr int AR_THREADS = 512;
+constexpr int AR_MAX_PEERS = 8;
+
+struct PeerPtrs {
+  float* p[AR_MAX_PEERS];
+};
+
+__global__ void __launch_bounds__(AR_THREADS)
+k_nvls_allreduce_f32(float* mc, int64_t n4, int rank, int world) {
+  const int64_t per = (n4 + world - 1) / world;
+  const int64_t b = static_cast<int64_t>(rank) * per;
+  const int64_t e = b + per < n4 ? b + per : n4;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * AR_THREADS;
+  for (int64_t i = b + static_cast<int64_t>(blockIdx.x) * AR_THREADS + threadIdx.x; i < e;
+       i += stride) {
+    float* a = mc + 4 * i;
+    uint32_t x, y, z, w;
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(x), "=r"(y), "=r"(z), "=r"(w)
+                 : "l"(a)
+                 : "memory");
+    asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(a), "r"(x),
+                 "r"(y), "r"(z), "r"(w)
+                 : "memory");
+  }
+}
+
+__global__ void __launch_bounds__(AR_THREADS)
+k_p2p_allreduce_f32(PeerPtrs peers, int64_t n4, int rank, int world) {
+  const int64_t per = (n4 + world - 1) / world;
+  const int64_t b = static_cast<int64_t>(rank) * per;
+  const int64_t e = b + per < n4 ? b + per : n4;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * AR_THREADS;
+  for (int64_t i = b + static_cast<int64_t>(blockIdx.x) * AR_THREADS + threadIdx.x; i < e;
+       i += stride) {
+    float4 s = reinterpret_cast<const float4*>(peers.p[0])[i];
+    for (int q = 1; q < world; ++q) {  // fixed rank order: deterministic
+      const float4 v = reinterpret_cast<const float4*>(peers.p[q])[i];
+      s.x += v.x;
+      s.y += v.y;
+      s.z += v.z;
+      s.w += v.w;
+    }
+    for (int q = 0; q < world; ++q) reinterpret_cast<float4*>(peers.p[q])[i] = s;
+  }
+}
+
+__global__ void __launch_bounds__(256)
+k_f32_rows_to_bf16(const float* __restrict__ src, int64_t R, int h, __nv_bfloat16* dst,
+                   int64_t ld) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  if (t >= R) return;
+  const float2* s = reinterpret_cast<const float2*>(src + t * h);
+  __nv_bfloat162* d = reinterpret_cast<__nv_bfloat162*>(dst + t * ld);
+  for (int k = threadIdx.x & 31; k < h / 2; k += 32) d[k] = __float22bfloat162_rn(s[k]);
+}
+
+}  // namespace rlh
+
+using namespace rlh;
+
+extern "C" {
+
+rl_status rl_allreduce_sum_f32(float* const* peer_ptrs, float* mc_ptr, int32_t rank,
+                               int32_t world, int64_t n, rl_stream_t stream) {
+  if (world < 1 || world > AR_MAX_PEERS || rank < 0 || rank >= world || n < 0 || (n & 3))
+    return RL_ERR_INVALID_ARG;
+  if (n == 0 || world == 1) return RL_OK;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int64_t n4 = n / 4;
+  const int64_t per = (n4 + world - 1) / world;
+  const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(per, AR_THREADS), 148 * 2));
+  TraceScope ts(RL_K_MISC, s);
+  if (mc_ptr) {
+    if ((reinterpret_cast<uintptr_t>(mc_ptr) & 15) != 0) return RL_ERR_INVALID_ARG;
+    k_nvls_allreduce_f32<<<blocks, AR_THREADS, 0, s>>>(mc_ptr, n4, rank, world);
+  } else {
+    if (!peer_ptrs) return RL_ERR_INVALID_ARG;
+    PeerPtrs pp{};
+    for (int q = 0; q < world; ++q) {
+      if (!peer_ptrs[q] || (reinterpret_cast<uintptr_t>(peer_ptrs[q]) & 15) != 0)
+        return RL_ERR_INVALID_ARG;
+      pp.p[q] = peer_ptrs[q];
+    }
+    k_p2p_allreduce_f32<<<blocks, AR_THREADS, 0, s>>>(pp, n4, rank, world);
+  }
+  RLH_CHECK_LAUNCH();
+  return RL_OK;
+}
+
+rl_status rl_cast_rows_bf16(const float* src, int64_t num_rows, int32_t hidden, void* dst,
+                            int64_t ld, rl_stream_t stream) {
+  if (num_rows < 0 || hidden < 2 || (hidden & 1) || ld < hidden || (ld & 1) ||
+      (num_rows > 0 && (!src || !dst)))
+    return RL_ERR_INVALID_ARG;
+  if (num_rows == 0) return RL_OK;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  TraceScope ts(RL_K_MISC, s);
+  k_f32_rows_to_bf16<<<static_cast<unsigned>(ceil_div(num_rows, 8)), 256, 0, s>>>(
+      src, num_rows, hidden, static_cast<__nv_bfloat16*>(dst), ld);
+  RLH_CHECK_LAUNCH();
+  return RL_OK;
+}
+
+}  // extern "C"

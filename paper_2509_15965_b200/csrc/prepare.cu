@@ -276,14 +276,15 @@ k_zero_inactive(char* __restrict__ out, int64_t ld_bytes, int64_t row_bytes, int
 }
 
 rl_status launch_zero_inactive(const rl_head* hd, void* grad_hidden, const WsLayout& L, char* ws,
-                               cudaStream_t s) {
+                               cudaStream_t s, bool f32_rows) {
   const uint8_t* act = reinterpret_cast<const uint8_t*>(ws + L.off_flags);
-  const int64_t esz = hd->dtype == RL_BF16 ? 2 : 4;
+  const int64_t esz = (hd->dtype == RL_BF16 && !f32_rows) ? 2 : 4;
+  const int64_t ld = f32_rows ? hd->hidden : hd->ld_hidden;
   const int64_t blocks = ceil_div(L.R, 8);
   if (blocks == 0) return RL_OK;
   TraceScope ts(RL_K_MISC, s);
   k_zero_inactive<<<static_cast<unsigned>(blocks), 256, 0, s>>>(
-      static_cast<char*>(grad_hidden), hd->ld_hidden * esz, static_cast<int64_t>(hd->hidden) * esz,
+      static_cast<char*>(grad_hidden), ld * esz, static_cast<int64_t>(hd->hidden) * esz,
       L.R, act);
   RLH_CHECK_LAUNCH();
   return RL_OK;

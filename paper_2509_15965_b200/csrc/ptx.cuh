@@ -162,6 +162,15 @@ __device__ __forceinline__ void st_global_v4_hint(void* p, uint4 v, uint64_t pol
                : "memory");
 }
 
+// NVLS: add four fp32 into every rank's copy behind a multicast address (the
+// NVSwitch performs the reduction; relaxed, system scope).
+__device__ __forceinline__ void multimem_red_add_v4_f32(void* mc, uint32_t a, uint32_t b,
+                                                        uint32_t c, uint32_t d) {
+  asm volatile("multimem.red.relaxed.sys.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(mc),
+               "r"(a), "r"(b), "r"(c), "r"(d)
+               : "memory");
+}
+
 // ------------------------------------------------- clusters / CTA pairs ----
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;

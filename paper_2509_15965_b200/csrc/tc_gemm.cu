@@ -92,6 +92,10 @@ struct TcArgs {
   __nv_bfloat16* out;
   int64_t ld_out;
   const int32_t* row_idx;
+  float* out_f32;      // non-NULL: fp32 rows [R, N] instead (vocab-parallel partial dL/dH
+                       // written straight into a symmetric NVLink-mapped buffer)
+  int32_t out_mc;      // out_f32 is an NVLS multicast address: multimem.red.add the tile
+                       // into every rank's copy (the TP all-reduce inside the epilogue)
   // EPI_ACC
   float* acc;
   int64_t ld_acc;
@@ -441,7 +445,22 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           tmem_ld_32x32b_x32(taddr + c * 32, v);
           tmem_ld_wait();
           if (c == C::TILE_N / 32 - 1) release(acc);
-          if (row_ok && n0 + c * 32 < args.N) {
+          if (args.out_f32) {
+            if (row_ok && n0 + c * 32 < args.N) {
+              float4* df = reinterpret_cast<float4*>(args.out_f32 + orow * args.N + n0 + c * 32);
+              if (args.out_mc) {
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                  multimem_red_add_v4_f32(df + q, v[4 * q], v[4 * q + 1], v[4 * q + 2],
+                                          v[4 * q + 3]);
+              } else {
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                  df[q] = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
+                                      __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
+              }
+            }
+          } else if (row_ok && n0 + c * 32 < args.N) {
             uint32_t pk[16];
 #pragma unroll
             for (int j = 0; j < 32; j += 2)
@@ -660,8 +679,8 @@ rl_status launch_tc_fwd(const rl_head* hd, const void* weight, const WsLayout& L
 }
 
 rl_status launch_tc_bwd(const rl_head* hd, const void* weight, void* grad_hidden,
-                        float* grad_weight, bool entropy_on, const WsLayout& L, char* ws,
-                        cudaStream_t s) {
+                        float* grad_hidden_f32, bool gh_multicast, float* grad_weight,
+                        bool entropy_on, const WsLayout& L, char* ws, cudaStream_t s) {
   const int h = hd->hidden, V = hd->vocab;
   const int cg = tc_cta_group();
   __nv_bfloat16* dz = reinterpret_cast<__nv_bfloat16*>(ws + L.off_dz);
@@ -703,6 +722,8 @@ rl_status launch_tc_bwd(const rl_head* hd, const void* weight, void* grad_hidden
   t6.N = h;
   t6.out = static_cast<__nv_bfloat16*>(grad_hidden);
   t6.ld_out = hd->ld_hidden;
+  t6.out_f32 = grad_hidden_f32;
+  t6.out_mc = gh_multicast ? 1 : 0;
   t6.row_idx = reinterpret_cast<const int32_t*>(ws + L.off_active);
   TcArgs t7 = base_args(hd, L, ws);
   t7.M = V;

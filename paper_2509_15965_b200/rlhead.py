@@ -88,7 +88,12 @@ lib.rl_logprob_merge.argtypes = [C.POINTER(rl_head), C.POINTER(rl_batch), _vp, C
 lib.rl_policy_loss_fwd_bwd_vp.restype = C.c_int
 lib.rl_policy_loss_fwd_bwd_vp.argtypes = [C.POINTER(rl_head), _vp, _vp, C.POINTER(rl_batch), _vp,
                                           C.c_int32, _vp, _vp, C.POINTER(rl_loss_params), _vp,
-                                          _vp, _vp, _vp, _vp, _vp, _sz, _vp]
+                                          _vp, _vp, C.c_int32, _vp, _vp, _vp, _sz, _vp]
+lib.rl_allreduce_sum_f32.restype = C.c_int
+lib.rl_allreduce_sum_f32.argtypes = [C.POINTER(C.c_void_p), _vp, C.c_int32, C.c_int32, C.c_int64,
+                                     _vp]
+lib.rl_cast_rows_bf16.restype = C.c_int
+lib.rl_cast_rows_bf16.argtypes = [_vp, C.c_int64, C.c_int32, _vp, C.c_int64, _vp]
 lib.rl_minibatch_early_stop.restype = C.c_int
 lib.rl_minibatch_early_stop.argtypes = [_vp, C.c_float, C.c_float, _vp, _vp, C.c_int64, _vp]
 lib.rl_scale_by_inverse_count.restype = C.c_int
@@ -117,7 +122,8 @@ EXPORTED = ["rl_workspace_size", "rl_batch_prepare", "rl_logprob_fwd", "rl_grpo_
             "rl_launch_count", "rl_trace_begin", "rl_trace_end", "rl_trace_durations",
             "rl_logprob_partials", "rl_logprob_merge", "rl_policy_loss_fwd_bwd_vp",
             "rl_minibatch_early_stop", "rl_scale_by_inverse_count", "rl_gae",
-            "rl_value_workspace_size", "rl_value_loss_fwd_bwd"]
+            "rl_value_workspace_size", "rl_value_loss_fwd_bwd", "rl_allreduce_sum_f32",
+            "rl_cast_rows_bf16"]
 
 
 class RLHeadError(RuntimeError):
@@ -306,18 +312,50 @@ def rl_logprob_merge(head: Head, batch: Batch, parts_all, logp, entropy=None, ls
 
 def rl_policy_loss_fwd_bwd_vp(head: Head, hidden, weight, batch: Batch, parts_all, old_logp, adv,
                               params: LossParams, logp, grad_hidden, grad_weight, entropy=None,
-                              stats=None, ws: Workspace | None = None, stream=None):
+                              stats=None, ws: Workspace | None = None, stream=None,
+                              grad_hidden_mc: int = 0):
     """Vocab-parallel phase 2 (training): grad_hidden is this shard's partial
-    dL/dH (all-reduce SUM over the TP group), grad_weight its rows of dL/dW."""
+    dL/dH (all-reduce SUM over the TP group), grad_weight its rows of dL/dW.
+    A float32 grad_hidden [R, hidden] selects the fp32 partial (for
+    rl_allreduce_sum_f32 over a symmetric buffer); grad_hidden_mc != 0 is the
+    multicast address of such a (zeroed) buffer: the epilogue adds into every
+    rank's copy (grad_hidden is then ignored)."""
+    import torch
     hd, b, p = head.c(), batch.c(), params.c()
     ws = ws or Workspace()
     buf = ws.get(rl_workspace_size(head, b.num_rows, True))
+    gh_f32 = int(grad_hidden is not None and grad_hidden.dtype == torch.float32
+                 and head.dtype == "bf16")
+    if grad_hidden_mc:
+        gh_f32, grad_hidden = 2, None
     _check(lib.rl_policy_loss_fwd_bwd_vp(C.byref(hd), _ptr(hidden), _ptr(weight), C.byref(b),
                                          _ptr(parts_all), int(parts_all.shape[0]), _ptr(old_logp),
                                          _ptr(adv), C.byref(p), _ptr(logp), _ptr(entropy),
-                                         _ptr(grad_hidden), _ptr(grad_weight), _ptr(stats),
+                                         C.c_void_p(int(grad_hidden_mc)) if grad_hidden_mc
+                                         else _ptr(grad_hidden), gh_f32, _ptr(grad_weight),
+                                         _ptr(stats),
                                          _ptr(buf), buf.numel(), _stream(stream)),
            "rl_policy_loss_fwd_bwd_vp")
+
+
+def rl_allreduce_sum_f32(buf, rank: int, world: int, peer_ptrs=None, mc_ptr: int = 0,
+                         stream=None):
+    """Sum buf (fp32, n % 4 == 0) over `world` ranks through NVLink peer memory:
+    NVLS multicast when mc_ptr != 0, else P2P over peer_ptrs (device addresses
+    of every rank's buf). The caller barriers before and after (symm_mem)."""
+    n = int(buf.numel())
+    arr = None
+    if not mc_ptr:
+        arr = (C.c_void_p * world)(*[int(x) for x in peer_ptrs])
+    _check(lib.rl_allreduce_sum_f32(arr, C.c_void_p(int(mc_ptr)) if mc_ptr else None, int(rank),
+                                    int(world), n, _stream(stream)), "rl_allreduce_sum_f32")
+
+
+def rl_cast_rows_bf16(src, dst, stream=None):
+    """dst[t, :h] = bf16(src[t, :h]) (src fp32 contiguous [R, h]; dst row stride any)."""
+    R, h = src.shape
+    _check(lib.rl_cast_rows_bf16(_ptr(src), int(R), int(h), _ptr(dst), int(dst.stride(0)),
+                                 _stream(stream)), "rl_cast_rows_bf16")
 
 
 def rl_minibatch_early_stop(stats, stop_flag, grad_weight, max_ratio: float = 0.0,

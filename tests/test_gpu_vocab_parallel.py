@@ -83,3 +83,80 @@ def test_vocab_parallel_emulated(rl, cfg, cuts, tol):
     dW = torch.cat(dW_rows).cpu().double().numpy()
     assert rel_fro(dH, refl["dH"]) <= g_tol
     assert rel_fro(dW, refl["dW"]) <= g_tol and max_rel(dW, refl["dW"]) <= max(g_tol, 1e-4)
+
+
+def test_vocab_parallel_fp32_partials_and_p2p_sum(rl):
+    """DESIGN.md §7.3 on one GPU: (a) the fp32 partial dL/dH (grad_hidden_fp32 = 1)
+    is the accumulator the bf16 path rounds -- bf16(fp32 rows) equals the bf16
+    rows bit for bit; (b) rl_allreduce_sum_f32 in P2P mode, driven once per
+    emulated rank over P buffers, leaves on every buffer the rank-order sum
+    ((s0 + s1) + s2 ... in fp32) bit-exactly; (c) that sum matches the oracle's
+    dL/dH and rl_cast_rows_bf16 rounds it to nearest-even like torch."""
+    import torch
+    cfg = SMALL_BF16
+    cuts = [0, 256, 512, 777, 1000]
+    lay = make_layout(cfg, seed=37)
+    H, W = make_tensors_host(cfg, lay.num_rows, seed=37)
+    d = dev_tensors(lay)
+    dev = "cuda"
+    R, V, h = lay.num_rows, cfg.vocab, cfg.hidden
+    Hd = H.to(dev)
+    batch = rl.Batch(d["cu"], d["targets"], d["mask"])
+    heads = [rl.Head(h, b - a, "bf16", vocab_offset=a, vocab_total=V)
+             for a, b in zip(cuts[:-1], cuts[1:])]
+    shards = [W[a:b].contiguous().to(dev) for a, b in zip(cuts[:-1], cuts[1:])]
+    P = len(heads)
+    parts = torch.zeros(P, 4, R, device=dev)
+    for i in range(P):
+        rl.rl_logprob_partials(heads[i], Hd, shards[i], batch, parts[i])
+    ref_f = oracle.logprob_fwd(H, W, lay.cu_seqlens, lay.mask, lay.targets)
+    adv, _ = oracle.grpo_advantage(lay.rewards, lay.group_of_seq, lay.num_groups)
+    adv = adv.astype(np.float32)
+    old = guarded_old_logp(ref_f["logp"], np.random.default_rng(4), band=1e-2)
+    N = lay.num_tokens
+    p = rl.LossParams(n_tokens_global=torch.tensor([N], device=dev))
+    old_d = torch.as_tensor(old, dtype=torch.float32, device=dev)
+    adv_d = torch.as_tensor(adv, device=dev)
+    bufs = []
+    for i in range(P):
+        lp = torch.empty(R, device=dev)
+        gh16 = torch.empty_like(Hd)
+        gh32 = torch.full((R, h), 7.0, device=dev)          # inactive rows must be zeroed
+        gw = torch.zeros(shards[i].shape[0], h, device=dev)
+        rl.rl_policy_loss_fwd_bwd_vp(heads[i], Hd, shards[i], batch, parts, old_d, adv_d, p, lp,
+                                     gh16, gw)
+        gw2 = torch.zeros_like(gw)
+        rl.rl_policy_loss_fwd_bwd_vp(heads[i], Hd, shards[i], batch, parts, old_d, adv_d, p, lp,
+                                     gh32, gw2)
+        torch.cuda.synchronize()
+        assert torch.equal(gh32.to(torch.bfloat16), gh16)                       # (a)
+        assert torch.equal(gw, gw2)
+        bufs.append(gh32)
+    expect = bufs[0].clone()
+    for q in range(1, P):
+        expect = expect + bufs[q]
+    ptrs = [b.data_ptr() for b in bufs]
+    for r in range(P):                                # each emulated rank sums its slice
+        rl.rl_allreduce_sum_f32(bufs[r], r, P, peer_ptrs=ptrs)
+    torch.cuda.synchronize()
+    for b in bufs:                                                              # (b)
+        assert torch.equal(b, expect)
+    refl = oracle.policy_loss_fwd_bwd(H, W, lay.cu_seqlens, lay.mask, lay.targets, old, adv,
+                                      n_global=N)
+    assert rel_fro(expect.cpu().double().numpy(), refl["dH"]) <= 1e-2                # (c)
+    out = torch.full((R, h + 64), 3.0, dtype=torch.bfloat16, device=dev)[:, :h]
+    rl.rl_cast_rows_bf16(expect, out)
+    torch.cuda.synchronize()
+    assert torch.equal(out, expect.to(torch.bfloat16))
+
+
+def test_allreduce_sum_f32_args(rl):
+    import torch
+    x = torch.ones(8, device="cuda")
+    rl.rl_allreduce_sum_f32(x, 0, 1, peer_ptrs=[x.data_ptr()])   # world 1: no-op
+    torch.cuda.synchronize()
+    assert torch.equal(x, torch.ones(8, device="cuda"))
+    with pytest.raises(rl.RLHeadError):
+        rl.rl_allreduce_sum_f32(torch.ones(6, device="cuda"), 0, 2, peer_ptrs=[x.data_ptr()] * 2)
+    with pytest.raises(rl.RLHeadError):
+        rl.rl_allreduce_sum_f32(x, 2, 2, peer_ptrs=[x.data_ptr()] * 2)

@@ -18,5 +18,5 @@ no printed number distinguishes them.
 from .head import (  # noqa: F401
     ERR_CU_SEQLENS, ERR_TARGET, ERR_GROUP,
     bookkeeping, logprob_fwd, grpo_group_stats, grpo_advantage,
-    grpo_advantage_from_stats, policy_loss_fwd_bwd, LossParams,
+    grpo_advantage_from_stats, batch_norm_advantage, policy_loss_fwd_bwd, LossParams,
 )

@@ -229,6 +229,52 @@ def grpo_advantage_from_stats(rewards, group_of_seq, sum_stats, max_stats, eps=1
     return adv
 
 
+def batch_norm_advantage(rewards, group_of_seq, num_groups, group_baseline=True, eps=1e-6,
+                         unbiased=True):
+    """REINFORCE++-style advantage, NEXT-1 (P:L654 names REINFORCE++ among the
+    supported algorithms; no formula is printed -- DESIGN.md §3 reading #33):
+    normalisation over the whole batch instead of per query.
+
+      x_s = r_s - mu_g(s)   (group_baseline; mu_g the plain mean of s's group)
+          = r_s             (otherwise)
+      A_s = (x_s - mean_B x) / (std_B x + eps)   over the sequences of the batch
+            with a valid group id (std over n-1 if unbiased else n);
+      A_s = 0 exactly when fewer than 2 valid sequences or max_B x == min_B x,
+      and for sequences with an invalid group id (ERR_GROUP).
+    Plain two-pass definition (means with math.fsum, then deviations)."""
+    r = _as64(rewards).reshape(-1)
+    gos = np.asarray(group_of_seq).reshape(-1)
+    S = r.shape[0]
+    adv = np.zeros(S)
+    err = 0
+    valid = [i for i in range(S) if 0 <= int(gos[i]) < num_groups]
+    if len(valid) < S:
+        err |= ERR_GROUP
+    x = {}
+    for i in valid:
+        x[i] = float(r[i])
+    if group_baseline:
+        for g in range(num_groups):
+            idx = [i for i in valid if int(gos[i]) == g]
+            if not idx:
+                continue
+            mu_g = math.fsum(float(r[i]) for i in idx) / len(idx)
+            for i in idx:
+                x[i] = float(r[i]) - mu_g
+    n = len(valid)
+    if n < 2:
+        return adv, err
+    xs = [x[i] for i in valid]
+    if max(xs) == min(xs):
+        return adv, err
+    mu = math.fsum(xs) / n
+    var = math.fsum((v - mu) ** 2 for v in xs) / ((n - 1) if unbiased else n)
+    sigma = math.sqrt(var)
+    for i in valid:
+        adv[i] = (x[i] - mu) / (sigma + eps)
+    return adv, err
+
+
 # --------------------------------------------------------------------------
 # H5: ratio, clipped surrogate, token-level mean; H6-H8: backward.
 # "Token-Level Loss: ... compute the average over tokens, as in DAPO" (P:L828);

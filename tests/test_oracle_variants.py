@@ -158,3 +158,71 @@ def test_minibatch_early_stop_rule():
     assert es(st, max_mean_ratio=1.1) and not es(st, max_mean_ratio=1.25)
     assert not es(st) and not es(dict(st, tokens=0), max_mean_ratio=1.0)
     assert not es(st, max_ratio=3.5)                 # strictly larger discards
+
+
+# ---- REINFORCE++-style batch-normalised advantage (DESIGN.md §3 #33) -------
+@pytest.mark.parametrize("Gn,G,k", [(1, 16, 5), (4, 8, 3), (8, 16, 1), (3, 4, 2)])
+def test_batch_adv_identical_groups_closed_form(Gn, G, k):
+    """Gn identical groups of G responses, k correct (+-5). With the
+    group baseline x_correct = 10(G-k)/G, x_wrong = -10k/G, mean_B x = 0 and
+    the unbiased batch variance is 100 Gn k(G-k)/G / (Gn G - 1), so
+    A_correct = sqrt((G-k)(Gn G-1) / (G k Gn)), A_wrong = -k/(G-k) A_correct
+    (Gn = 1 reduces to GRPO's unbiased P6). Without the baseline the batch is
+    one pool of Gn*k correct of Gn*G: P6 with G -> Gn G."""
+    r = np.array(([5.0] * k + [-5.0] * (G - k)) * Gn, dtype=np.float32)
+    gos = np.repeat(np.arange(Gn), G).astype(np.int32)
+    A, err = oracle.batch_norm_advantage(r, gos, Gn, group_baseline=True, eps=0.0)
+    assert err == 0
+    ac = math.sqrt((G - k) * (Gn * G - 1) / (G * k * Gn))
+    np.testing.assert_allclose(A[r > 0], ac, rtol=1e-12)
+    np.testing.assert_allclose(A[r < 0], -k / (G - k) * ac, rtol=1e-12)
+    if Gn == 1:
+        Ag, _ = oracle.grpo_advantage(r, gos, 1, eps=0.0)
+        np.testing.assert_allclose(A, Ag, rtol=1e-12)
+    n = Gn * G
+    A, _ = oracle.batch_norm_advantage(r, gos, Gn, group_baseline=False, eps=0.0, unbiased=False)
+    kk = Gn * k
+    np.testing.assert_allclose(A[r > 0], math.sqrt((n - kk) / kk), rtol=1e-12)
+    np.testing.assert_allclose(A[r < 0], -math.sqrt(kk / (n - kk)), rtol=1e-12)
+
+
+def test_batch_adv_invariants():
+    """sum_B A = 0, sum_B A^2 = n-1 (unbiased) / n (population), eps = 0; the
+    group baseline makes A invariant to shifting one group's rewards, the
+    no-baseline form is not; both are invariant to a global affine map."""
+    rng = np.random.default_rng(8)
+    r = rng.normal(size=40)
+    gos = rng.integers(0, 5, size=40).astype(np.int32)
+    for gb in (True, False):
+        for unbiased, want in [(True, 39.0), (False, 40.0)]:
+            A, _ = oracle.batch_norm_advantage(r, gos, 5, group_baseline=gb, eps=0.0,
+                                               unbiased=unbiased)
+            assert abs(A.sum()) < 1e-12
+            assert (A ** 2).sum() == pytest.approx(want, rel=1e-12)
+        A0, _ = oracle.batch_norm_advantage(r, gos, 5, group_baseline=gb, eps=0.0)
+        A1, _ = oracle.batch_norm_advantage(3.0 * r - 2.0, gos, 5, group_baseline=gb, eps=0.0)
+        np.testing.assert_allclose(A1, A0, rtol=1e-10, atol=1e-12)
+        r2 = r.copy()
+        r2[gos == 2] += 7.0
+        A2, _ = oracle.batch_norm_advantage(r2, gos, 5, group_baseline=gb, eps=0.0)
+        assert np.allclose(A2, A0, rtol=1e-10, atol=1e-12) == gb
+
+
+def test_batch_adv_degenerate_and_invalid():
+    """A = 0 exactly: every group zero-variance under the baseline (all x = 0),
+    a single valid sequence, an all-equal batch without baseline. Invalid group
+    ids get A = 0, raise ERR_GROUP and are left out of the batch statistics."""
+    r = np.array([0.7] * 7 + [5, 5, 5], dtype=np.float32)
+    gos = np.array([0] * 7 + [1] * 3, dtype=np.int32)
+    A, err = oracle.batch_norm_advantage(r, gos, 2, group_baseline=True)
+    assert err == 0 and (A == 0.0).all()
+    A, _ = oracle.batch_norm_advantage(np.array([3.0], np.float32), np.array([0], np.int32), 1)
+    assert (A == 0.0).all()
+    A, _ = oracle.batch_norm_advantage(np.full(6, 2.5, np.float32), np.zeros(6, np.int32), 1,
+                                       group_baseline=False)
+    assert (A == 0.0).all()
+    r = np.array([5, -5, 5, -5, 100.0], dtype=np.float32)
+    gos = np.array([0, 0, 1, 1, 9], dtype=np.int32)
+    A, err = oracle.batch_norm_advantage(r, gos, 2, group_baseline=False, eps=0.0, unbiased=False)
+    assert err == oracle.ERR_GROUP and A[4] == 0.0
+    np.testing.assert_allclose(A[:4], [1, -1, 1, -1], rtol=1e-12)

@@ -46,6 +46,11 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample-tokens", type=int, default=512)
+    p.add_argument("--collective", default="symm", choices=["symm", "nccl"],
+                   help="N>1 dW reduction: reduce-scatter fused into the last dW GEMM epilogue "
+                        "+ NVLink all-gather (symm), or NCCL all-reduce")
+    p.add_argument("--no-aux", action="store_true",
+                   help="skip the auxiliary lines (forward-only path, HBM kernels)")
     return p.parse_args()
 
 
@@ -219,7 +224,14 @@ def main():
     old += torch.as_tensor(ratio_noise(old.shape[0], args.seed + rank), dtype=torch.float32,
                            device=dev)
     del ws
-    step = PolicyLossStep(head, W, db, group=group)
+    collective = args.collective if world > 1 else "none"
+    try:
+        step = PolicyLossStep(head, W, db, group=group,
+                              collective="symm" if collective == "symm" else "nccl")
+    except Exception as e:  # symmetric memory unavailable: NCCL all-reduce instead
+        print(f"[bench] collective=symm unavailable ({e}); using nccl", file=sys.stderr)
+        collective = "nccl"
+        step = PolicyLossStep(head, W, db, group=group, collective="nccl")
     gh = torch.empty(max_mb, cfg.hidden, dtype=H.dtype, device=dev)
     tokens_local = int(sum(int(mine.mask[r0:r1].sum()) for _, _, r0, r1, _ in db.mbs))
     tok_t = torch.tensor([tokens_local], dtype=torch.int64, device=dev)
@@ -284,6 +296,12 @@ def main():
             "step_executed_frac_burst": round(step_tflops_exec / world / pk["bf16"], 4),
             "step_algorithmic_frac_burst": round(step_tflops_alg / world / pk["bf16"], 4)}
 
+    # ------------------------------------ auxiliary measurements (M.1, M.4)
+    aux = None
+    if not args.no_aux:
+        aux = run_aux(rl, head, H, W, db, mine, step, kinds, tokens_local, tokens_global, cfg,
+                      pk, world, args.steps)
+
     # ------------------------------------------------ end-to-end (host data)
     e2e = None
     if not args.no_e2e:
@@ -303,17 +321,92 @@ def main():
                                    f"{cfg.prompts} prompts x G={cfg.group}, responses <= {cfg.lmax}",
                        "global_batch_tokens": tokens_global, "micro_batch_rows": args.mb_rows,
                        "micro_batches_per_rank": len(db.mbs), "parallelism": f"dp{world}",
+                       "dw_collective": collective,
                        "l2": "inputs > L2 (hidden rows of the mini-batch ~ "
                              f"{mine.num_rows * cfg.hidden * 2 / 1e9:.1f} GB per rank)",
                        "lpt_load_max_over_mean": round(float(loads.max() / loads.mean()), 4),
                        "partial": bool(args.max_mb)},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-            "clocks": clocks, "kernels": per_kind,
+            "clocks": clocks, "kernels": per_kind, "aux": aux,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def run_aux(rl, head, H, W, db, mine, step, kinds, tokens_local, tokens_global, cfg, pk, world,
+            steps):
+    """SURVEY M.1/M.4 side numbers (not the headline):
+    * fwd_only: the inference-worker path (rl_logprob_fwd over every micro-
+      batch: H1 + H3 + H4), tokens/s, device time, max over ranks;
+    * bookkeeping: H1 (rl_batch_prepare) once over the rank's whole mini-batch
+      (all packed rows in one call), algorithmic bytes / time vs the HBM peak;
+    * merge: the H4-merge + H5 kernel inside the timed steps (live per-launch
+      events), algorithmic bytes 12 n_vt + 30 per active row."""
+    import torch
+    import torch.distributed as dist
+    dev = H.device
+
+    def max_ms(x):
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    out = {}
+    ws = step.ws
+    lp = step.logp
+    mb0 = db.mbs[0]
+    rl.rl_logprob_fwd(head, H[mb0[2]:mb0[3]], W, rl.Batch(mb0[4], db.targets[mb0[2]:mb0[3]],
+                      db.mask[mb0[2]:mb0[3]], num_rows=mb0[3] - mb0[2]), lp[mb0[2]:mb0[3]], ws=ws)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for (s0, s1, r0, r1, cu_mb) in db.mbs:
+        rl.rl_logprob_fwd(head, H[r0:r1], W, rl.Batch(cu_mb, db.targets[r0:r1], db.mask[r0:r1],
+                                                      num_rows=r1 - r0), lp[r0:r1], ws=ws)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = max_ms(e0.elapsed_time(e1))
+    fwd_tflops = 2.0 * cfg.hidden * cfg.vocab * tokens_global / (ms / 1e3) / 1e12 / world
+    out["fwd_only"] = {"metric": "logprob fwd tokens/s (inference worker)",
+                       "value": round(tokens_global / (ms / 1e3), 1), "unit": "tokens/s",
+                       "ms": round(ms, 3), "tflops_per_gpu": round(fwd_tflops, 1),
+                       "frac_of_burst": round(fwd_tflops / pk["bf16"], 4)}
+    # H1 over the whole local mini-batch
+    R = mine.num_rows
+    S = int(db.cu.shape[0]) - 1
+    row_seq = torch.empty(max(R, 1), dtype=torch.int32, device=dev)
+    act = torch.empty(max(R, 1), dtype=torch.int32, device=dev)
+    na = torch.zeros(1, dtype=torch.int64, device=dev)
+    wsp = rl.Workspace(dev)
+    b = rl.Batch(db.cu, db.targets, db.mask)
+    rl.rl_batch_prepare(head, b, row_seq=row_seq, active_idx=act, n_active=na, ws=wsp)
+    torch.cuda.synchronize()
+    reps = 5
+    e0.record()
+    for _ in range(reps):
+        rl.rl_batch_prepare(head, b, row_seq=row_seq, active_idx=act, n_active=na, ws=wsp)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = max_ms(e0.elapsed_time(e1) / reps)
+    T = int(mine.num_tokens)
+    nbytes = R * (4 + 1 + 4) + 4 * (S + 1) + 4 * T   # targets+mask in, row_seq out, cu, active out
+    gbs = nbytes / (ms / 1e3) / 1e9
+    out["bookkeeping"] = {"rows": R, "ms": round(ms, 4), "bytes": nbytes, "gbs": round(gbs, 1),
+                          "frac_hbm": round(gbs / pk["hbm"], 4),
+                          "note": "H1 once over the rank's whole mini-batch; bytes algorithmic"}
+    del wsp
+    if "merge" in kinds:
+        n, t = kinds["merge"]
+        n_vt = -(-cfg.vocab // 256)
+        nb = (12 * n_vt + 30) * tokens_local * steps
+        g = nb / (t / 1e3) / 1e9
+        out["merge"] = {"launches": n, "ms_per_launch": round(t / max(n, 1), 4),
+                        "gbs": round(g, 1), "frac_hbm": round(g / pk["hbm"], 4),
+                        "bytes_per_token": 12 * n_vt + 30}
+    return out
 
 
 def run_e2e(args, rl, step, db, mine, H, old, gh, dev, world, tokens_global):

@@ -139,6 +139,34 @@ RL_API rl_status rl_grpo_advantage(const float *rewards, const int32_t *group_of
                             const double *max_stats, float eps, int32_t unbiased, float *adv,
                             int32_t *err_flags, rl_stream_t stream);
 
+/* Debug helper (the only call that synchronises): copy the device error word
+ * err_flags (RL_DEVERR_* bits, OR-ed by the calls that were given it) into
+ * *host_code after everything queued on `stream` has finished. */
+RL_API rl_status rl_read_device_error(const int32_t *err_flags, int32_t *host_code,
+                                      rl_stream_t stream);
+
+/* REINFORCE++-style batch-normalised advantage (NEXT-1; P:L654 names
+ * REINFORCE++, no formula; DESIGN.md §3 #33):
+ *   x_s = r_s - mu_g(s)  if group_baseline (mu_g = n_g^-1 sum r from
+ *                         group_sum_stats, as rl_grpo_group_stats writes it,
+ *                         all-reduced if groups are split), else x_s = r_s;
+ *   A_s = (x_s - mean_B x) / (std_B x + eps) over the batch's sequences with a
+ *         valid group id (std over n-1 if unbiased else n); A_s = 0 exactly
+ *         when n <= 1 or max x == min x, and for invalid ids (RL_DEVERR_GROUP;
+ *         group_of_seq may be NULL without baseline: every sequence valid).
+ * Batch statistics fp64 [5] = (n, sum x, sum x^2, max x, -min x):
+ *   batch_stats_out != NULL: this call's local statistics are written there
+ *     (multi-rank: call with adv = NULL, all-reduce SUM [0:3] / MAX [3:5],
+ *     then call again with batch_stats_in);
+ *   batch_stats_in != NULL: A uses these instead of the local ones.
+ * adv [num_seqs] fp32 out (may be NULL when only statistics are wanted). */
+RL_API rl_status rl_batch_norm_advantage(const float *rewards, const int32_t *group_of_seq,
+                                         int32_t num_seqs, int32_t num_groups,
+                                         int32_t group_baseline, const double *group_sum_stats,
+                                         const double *batch_stats_in, double *batch_stats_out,
+                                         float eps, int32_t unbiased, float *adv,
+                                         int32_t *err_flags, rl_stream_t stream);
+
 /* Loss parameters (host struct; DESIGN.md §3 #12-#15, NEXT-1 variants
  * #25-#28). Per active token t of sequence s with weight w_t:
  *   L += w_t (l_t + kl_coef * k3_t - entropy_coef * H_t)
@@ -164,7 +192,33 @@ typedef struct {
   const int64_t *n_seqs_global;   /* device: S (seq_mean); see rl_batch_prepare      */
   int32_t adv_per_token;          /* 0: adv is [S] per sequence (GRPO); 1: adv is [R]
                                      per row (PPO/GAE, NEXT-4)                        */
+  const struct rl_peer_group *dw_reduce_scatter; /* NULL: grad_weight += locally.
+                                     Else (the LAST micro-batch of a mini-batch on
+                                     every DP rank; bf16 tensor-core path): see
+                                     rl_peer_group                                     */
 } rl_loss_params;
+
+/* DP reduction of dW fused into the last micro-batch's dW GEMM (C3 of
+ * SURVEY §8(e)). grad_weight [V][h] fp32 (ld = h) lives in
+ * memory every rank of the group has mapped (symmetric memory); rows are
+ * owned in slabs: owner(j) = min(j / rows_per_rank, world - 1). With
+ * params->dw_reduce_scatter set, the dW epilogue adds, for every finished
+ * tile, (this rank's accumulated partial + the tile) into the OWNER's
+ * grad_weight with red.add over NVLink (the owner adds its own tile in
+ * place), so the reduce-scatter overlaps the GEMM tile by tile. After the
+ * call returned on every rank and a cross-rank barrier, rows owned by rank
+ * r hold the SUM over ranks in rank r's buffer (fp32 atomics: the order of
+ * the adds is not fixed); the other rows of a buffer keep that rank's local
+ * partial. rl_allgather_rows_f32 then broadcasts each slab (all-reduce).
+ * The caller zeroes every rank's grad_weight and barriers before any rank
+ * starts that mini-batch's last micro-batch. */
+typedef struct rl_peer_group {
+  int32_t rank;                   /* this rank in the group                          */
+  int32_t world;                  /* 1..8                                            */
+  int64_t rows_per_rank;          /* > 0                                             */
+  float *peers[8];                /* device: every rank's grad_weight, peers[rank]
+                                     == this call's grad_weight                      */
+} rl_peer_group;
 
 /* Loss statistics, device resident, ACCUMULATED (+=) by every call. The
  * caller zeroes it at the start of a mini-batch. Raw sums over active rows:
@@ -309,6 +363,15 @@ RL_API rl_status rl_policy_loss_fwd_bwd_vp(const rl_head *hd, const void *hidden
  * 1 <= world <= 8, else RL_ERR_INVALID_ARG; world == 1 is a no-op. */
 RL_API rl_status rl_allreduce_sum_f32(float *const *peer_ptrs, float *mc_ptr, int32_t rank,
                                       int32_t world, int64_t n, rl_stream_t stream);
+/* All-gather of row slabs over NVLink peer memory: rank `rank` broadcasts
+ * its owned rows [rank*rows_per_rank, min((rank+1)*rows_per_rank, num_rows))
+ * (the last rank owns through num_rows) of buf [num_rows][cols] fp32 to
+ * every rank's buf -- multimem.st through the multicast address mc_ptr when
+ * given, else plain stores to peer_ptrs (HOST array of world device
+ * pointers). Bracket with cross-rank barriers. cols % 4 == 0. */
+RL_API rl_status rl_allgather_rows_f32(float *const *peer_ptrs, float *mc_ptr, int32_t rank,
+                                       int32_t world, int64_t num_rows, int64_t cols,
+                                       int64_t rows_per_rank, rl_stream_t stream);
 /* dst[t][0:hidden] (bf16, row stride ld) = round-to-nearest(src[t][0:hidden])
  * (fp32, row stride hidden), t < num_rows; hidden even, ld >= hidden even. */
 RL_API rl_status rl_cast_rows_bf16(const float *src, int64_t num_rows, int32_t hidden, void *dst,

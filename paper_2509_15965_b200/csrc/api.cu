@@ -56,7 +56,7 @@ bool ws_layout(const rl_head* hd, int64_t R, int want_bwd, WsLayout* L) {
   L->n_vt = tc ? ceil_div(V, TC_BN) : 1;
   L->Vp = round_up(V, TC_BN);
   L->nblk_rows = ceil_div(R, 1024);
-  L->nblk_loss = ceil_div(L->Rp, 256);
+  L->nblk_loss = ceil_div(L->Rp, 32);  // k_merge: 32 rows per block
   size_t o = 0;
   auto take = [&](size_t bytes) {
     const size_t at = o;
@@ -265,6 +265,32 @@ rl_status rl_grpo_advantage(const float* rewards, const int32_t* group_of_seq, i
                      reinterpret_cast<cudaStream_t>(stream));
 }
 
+rl_status rl_read_device_error(const int32_t* err_flags, int32_t* host_code,
+                               rl_stream_t stream) {
+  if (!err_flags || !host_code) return RL_ERR_INVALID_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (cudaMemcpyAsync(host_code, err_flags, sizeof(int32_t), cudaMemcpyDeviceToHost, s) !=
+          cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess)
+    return RL_ERR_CUDA;
+  return RL_OK;
+}
+
+rl_status rl_batch_norm_advantage(const float* rewards, const int32_t* group_of_seq,
+                                  int32_t num_seqs, int32_t num_groups, int32_t group_baseline,
+                                  const double* group_sum_stats, const double* batch_stats_in,
+                                  double* batch_stats_out, float eps, int32_t unbiased,
+                                  float* adv, int32_t* err_flags, rl_stream_t stream) {
+  if (num_seqs < 0 || num_groups < 0 || !(eps >= 0.f)) return RL_ERR_INVALID_ARG;
+  if (group_baseline != 0 && group_baseline != 1) return RL_ERR_INVALID_ARG;
+  if (group_baseline && (!group_of_seq || !group_sum_stats)) return RL_ERR_INVALID_ARG;
+  if (!adv && !batch_stats_out) return RL_ERR_INVALID_ARG;
+  if (num_seqs > 0 && !rewards) return RL_ERR_INVALID_ARG;
+  return launch_batch_adv(rewards, group_of_seq, num_seqs, num_groups, group_baseline,
+                          group_sum_stats, batch_stats_in, batch_stats_out, eps, unbiased, adv,
+                          err_flags, reinterpret_cast<cudaStream_t>(stream));
+}
+
 }  // extern "C"
 
 // Training-worker path (H1-H8). parts_all == NULL: the softmax is finished
@@ -291,6 +317,14 @@ static rl_status loss_impl(const rl_head* hd, const void* hidden, const void* we
     return RL_ERR_INVALID_ARG;
   if (p->adv_per_token && b->num_rows > 0 && !adv) return RL_ERR_INVALID_ARG;
   if (p->kl_coef > 0.f && b->num_rows > 0 && !p->ref_logp) return RL_ERR_INVALID_ARG;
+  const rl_peer_group* rs = p->dw_reduce_scatter;
+  if (rs) {
+    if (rs->world < 1 || rs->world > 8 || rs->rank < 0 || rs->rank >= rs->world ||
+        rs->rows_per_rank <= 0 || rs->peers[rs->rank] != grad_weight)
+      return RL_ERR_INVALID_ARG;
+    for (int q = 0; q < rs->world; ++q)
+      if (!rs->peers[q] || !aligned(rs->peers[q], 16)) return RL_ERR_INVALID_ARG;
+  }
   const bool entropy_on = p->entropy_coef > 0.f;
   WsLayout L;
   ws_layout(hd, b->num_rows, 1, &L);
@@ -302,6 +336,7 @@ static rl_status loss_impl(const rl_head* hd, const void* hidden, const void* we
   if (gh_f32 && (hd->dtype == RL_BF16 ? !tc : hd->ld_hidden != hd->hidden))
     return RL_ERR_INVALID_ARG;
   if (gh_mc && !tc) return RL_ERR_INVALID_ARG;
+  if (rs && !tc) return RL_ERR_INVALID_ARG;
   if (tc && (!aligned(hidden, 16) || !aligned(weight, 16) || !aligned(grad_hidden, 16) ||
              !aligned(grad_weight, 16)))
     return RL_ERR_INVALID_ARG;
@@ -361,7 +396,7 @@ static rl_status loss_impl(const rl_head* hd, const void* hidden, const void* we
   if (tc)
     return launch_tc_bwd(hd, weight, gh_f32 ? nullptr : grad_hidden,
                          gh_f32 ? static_cast<float*>(grad_hidden) : nullptr, gh_mc,
-                         grad_weight, entropy_on, L, w, s);
+                         grad_weight, rs, entropy_on, L, w, s);
   return launch_simt_bwd(hd, hidden, weight, grad_hidden, grad_weight, entropy_on, L, w, s);
 }
 

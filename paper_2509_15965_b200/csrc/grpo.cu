@@ -105,4 +105,84 @@ rl_status launch_grpo(const float* rewards, const int32_t* gos, int32_t S, int32
   return RL_OK;
 }
 
+// NEXT-1, REINFORCE++-style batch normalisation (DESIGN.md §3 #33):
+// x_s = r_s - mu_g(s) (group baseline, mu from the given group sums) or r_s;
+// A_s = (x_s - mean_B x) / (std_B x + eps) over the valid sequences. One CTA:
+// each thread accumulates its strided members in index order, then the fixed-
+// order block reduction above (deterministic fp64). bin != NULL: the batch
+// statistics (n, sum x, sum x^2, max x, -min x) were all-reduced by the
+// caller; bout != NULL: write this call's local ones.
+__device__ __forceinline__ bool bn_x(const float* r, const int32_t* gos, int32_t G, int32_t gb,
+                                     const double* gsum, int i, double* x) {
+  double v = static_cast<double>(r[i]);
+  if (gos) {
+    const int32_t g = gos[i];
+    if (g < 0 || g >= G) return false;
+    if (gb) {
+      const double n = gsum[3 * g];
+      v = n > 0.0 ? v - gsum[3 * g + 1] / n : 0.0;
+    }
+  }
+  *x = v;
+  return true;
+}
+
+__global__ void __launch_bounds__(GRPO_THREADS)
+k_batch_adv(const float* __restrict__ r, const int32_t* __restrict__ gos, int32_t S, int32_t G,
+            int32_t gb, const double* __restrict__ gsum, const double* __restrict__ bin,
+            double* __restrict__ bout, float eps, int32_t unbiased, float* __restrict__ adv,
+            int32_t* err) {
+  GStat st;
+  int bad = 0;
+  if (!bin || bout) {
+    GStat v{0.0, 0.0, 0.0, -INFINITY, -INFINITY};
+    for (int i = threadIdx.x; i < S; i += GRPO_THREADS) {
+      double x;
+      if (!bn_x(r, gos, G, gb, gsum, i, &x)) {
+        bad = 1;
+        continue;
+      }
+      v.n += 1.0;
+      v.s1 += x;
+      v.s2 += x * x;
+      v.mx = fmax(v.mx, x);
+      v.nmn = fmax(v.nmn, -x);
+    }
+    st = block_reduce_gstat(v);
+  }
+  bad = __syncthreads_or(bad);
+  if (threadIdx.x == 0 && bad && err) atomicOr(err, RL_DEVERR_GROUP);
+  if (bout && threadIdx.x == 0) {
+    bout[0] = st.n;
+    bout[1] = st.s1;
+    bout[2] = st.s2;
+    bout[3] = st.mx;
+    bout[4] = st.nmn;
+  }
+  if (!adv) return;
+  if (bin) st = {bin[0], bin[1], bin[2], bin[3], bin[4]};
+  const bool degenerate = (st.n <= 1.0) || (st.mx == -st.nmn);
+  const double mu = st.n > 0 ? st.s1 / st.n : 0.0;
+  double var = st.s2 - st.n * mu * mu;
+  var = var > 0.0 ? var : 0.0;
+  var /= unbiased ? (st.n - 1.0) : st.n;
+  const double denom = sqrt(var) + static_cast<double>(eps);
+  for (int i = threadIdx.x; i < S; i += GRPO_THREADS) {
+    double x;
+    const bool ok = bn_x(r, gos, G, gb, gsum, i, &x);
+    adv[i] = (!ok || degenerate) ? 0.f : static_cast<float>((x - mu) / denom);
+  }
+}
+
+rl_status launch_batch_adv(const float* rewards, const int32_t* gos, int32_t S, int32_t G,
+                           int32_t group_baseline, const double* gsum, const double* bin,
+                           double* bout, float eps, int32_t unbiased, float* adv, int32_t* err,
+                           cudaStream_t s) {
+  TraceScope ts(RL_K_GRPO, s);
+  k_batch_adv<<<1, GRPO_THREADS, 0, s>>>(rewards, gos, S, G, group_baseline, gsum, bin, bout, eps,
+                                         unbiased, adv, err);
+  RLH_CHECK_LAUNCH();
+  return RL_OK;
+}
+
 }  // namespace rlh

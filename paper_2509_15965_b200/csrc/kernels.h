@@ -24,6 +24,10 @@ rl_status launch_grpo(const float* rewards, const int32_t* gos, int32_t S, int32
                       const double* sum_in, const double* max_in, float eps, int32_t unbiased,
                       float* adv, double* sum_out, double* max_out, int32_t* err,
                       cudaStream_t s);
+rl_status launch_batch_adv(const float* rewards, const int32_t* gos, int32_t S, int32_t G,
+                           int32_t group_baseline, const double* gsum, const double* bin,
+                           double* bout, float eps, int32_t unbiased, float* adv, int32_t* err,
+                           cudaStream_t s);
 
 // H4 merge of the split-V partials (+ H5 loss when old_logp != NULL).
 struct MergeArgs {
@@ -77,7 +81,8 @@ rl_status launch_tc_fwd(const rl_head* hd, const void* weight, const WsLayout& L
 // multicast address and the rows are added into every rank's copy.
 rl_status launch_tc_bwd(const rl_head* hd, const void* weight, void* grad_hidden,
                         float* grad_hidden_f32, bool gh_multicast, float* grad_weight,
-                        bool entropy_on, const WsLayout& L, char* ws, cudaStream_t s);
+                        const rl_peer_group* dw_rs, bool entropy_on, const WsLayout& L, char* ws,
+                        cudaStream_t s);
 
 int num_sms();
 

@@ -14,6 +14,8 @@
 namespace rlh {
 
 constexpr int MERGE_THREADS = 256;
+constexpr int MERGE_ROWS = 32;                     // k_merge rows per block
+constexpr int MERGE_SPLIT = MERGE_THREADS / 32;    // warps splitting the partials
 
 struct LStat {
   double loss, ratio, ent, kl, obj;
@@ -73,27 +75,60 @@ __device__ __forceinline__ int64_t lower_bound_rows(const int32_t* __restrict__ 
   return lo;
 }
 
+// Fold one partial (m, s, u) into the running (M, S, U); M = -inf = empty.
+__device__ __forceinline__ void lse_fold(float& M, float& S, float& U, float m, float s, float u) {
+  if (M == -INFINITY) {
+    M = m;
+    S = s;
+    U = u;
+    return;
+  }
+  if (m > M) {  // rescale the running sums to the new max
+    const float f = expf(M - m);
+    U = f * (U + (M - m) * S);
+    S = f * S;
+    M = m;
+  }
+  const float f2 = expf(m - M);
+  S += s * f2;
+  U += f2 * (u + (m - M) * s);
+}
+
+// Block = MERGE_ROWS rows x MERGE_SPLIT warps: lane = row (coalesced 128-B
+// loads of the SoA partials), warp w folds its contiguous chunk of the n_vt
+// partials; warp 0 then folds the MERGE_SPLIT chunk results in warp order
+// (fixed, deterministic) and runs the per-row loss. 8x the loads in flight of
+// a thread-per-row loop, which left the kernel latency-bound.
 template <bool LOSS>
 __global__ void __launch_bounds__(MERGE_THREADS)
 k_merge(MergeArgs a, const WsHeader* __restrict__ hdr, int64_t ldp) {
+  __shared__ float sh_m[MERGE_SPLIT][MERGE_ROWS], sh_s[MERGE_SPLIT][MERGE_ROWS],
+      sh_u[MERGE_SPLIT][MERGE_ROWS];
   const int64_t T = hdr->n_active;
-  const int64_t r = static_cast<int64_t>(blockIdx.x) * MERGE_THREADS + threadIdx.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * MERGE_ROWS + lane;
   const int64_t n_vt = a.nparts, pst = a.part_stride;
+  {
+    float M = -INFINITY, S = 0.f, U = 0.f;
+    if (r < T) {
+      const int64_t per = (n_vt + MERGE_SPLIT - 1) / MERGE_SPLIT;
+      const int64_t n0 = wid * per, n1 = n0 + per < n_vt ? n0 + per : n_vt;
+#pragma unroll 4
+      for (int64_t n = n0; n < n1; ++n)
+        lse_fold(M, S, U, a.pm[n * pst + r], a.ps[n * pst + r], a.pu[n * pst + r]);
+    }
+    sh_m[wid][lane] = M;
+    sh_s[wid][lane] = S;
+    sh_u[wid][lane] = U;
+  }
+  __syncthreads();
+  if (wid != 0) return;
   LStat st{0.0, 0.0, 0.0, 0.0, 0.0, 0.f, 0, 0, 0};
   if (r < T) {
-    float M = a.pm[r], S = a.ps[r], U = a.pu[r];
-    for (int64_t n = 1; n < n_vt; ++n) {
-      const float m = a.pm[n * pst + r], s = a.ps[n * pst + r], u = a.pu[n * pst + r];
-      if (m > M) {  // rescale the running sums to the new max
-        const float f = expf(M - m);
-        U = f * (U + (M - m) * S);
-        S = f * S;
-        M = m;
-      }
-      const float f2 = expf(m - M);
-      S += s * f2;
-      U += f2 * (u + (m - M) * s);
-    }
+    float M = -INFINITY, S = 0.f, U = 0.f;
+#pragma unroll
+    for (int w = 0; w < MERGE_SPLIT; ++w)
+      if (sh_m[w][lane] != -INFINITY) lse_fold(M, S, U, sh_m[w][lane], sh_s[w][lane], sh_u[w][lane]);
     if (a.parts_out) {  // vocab-parallel phase 1: this shard's merged partial
       const int64_t yl = static_cast<int64_t>(a.tgt_c[r]) - a.y_off;
       a.parts_out[r] = M;
@@ -172,7 +207,11 @@ k_merge(MergeArgs a, const WsHeader* __restrict__ hdr, int64_t ldp) {
     }
   }
   if constexpr (LOSS) {
-    st = block_reduce_lstat<MERGE_THREADS>(st);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {  // warp 0 only: fixed-order butterfly
+      LStat w = lstat_shfl(st, o);
+      lstat_add(st, w);
+    }
     if (threadIdx.x == 0) {
       a.st_d[5 * blockIdx.x] = st.loss;
       a.st_d[5 * blockIdx.x + 1] = st.ratio;
@@ -219,7 +258,7 @@ rl_status launch_zy_combine(const float* parts_all, int64_t nparts, int64_t ldr,
                             const WsLayout& L, char* ws, cudaStream_t s) {
   if (L.nblk_loss == 0) return RL_OK;
   TraceScope ts(RL_K_MERGE, s);
-  k_zy_combine<<<static_cast<unsigned>(L.nblk_loss), MERGE_THREADS, 0, s>>>(
+  k_zy_combine<<<static_cast<unsigned>(ceil_div(L.Rp, MERGE_THREADS)), MERGE_THREADS, 0, s>>>(
       parts_all, nparts, ldr, reinterpret_cast<const WsHeader*>(ws + L.off_hdr),
       reinterpret_cast<float*>(ws + L.off_zy));
   RLH_CHECK_LAUNCH();

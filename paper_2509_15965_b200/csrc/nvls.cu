@@ -61,6 +61,30 @@ k_p2p_allreduce_f32(PeerPtrs peers, int64_t n4, int rank, int world) {
   }
 }
 
+// All-gather of this rank's slab [b, e) (float4 units): multicast or P2P.
+__global__ void __launch_bounds__(AR_THREADS)
+k_nvls_bcast_f32(const float* __restrict__ local, float* mc, int64_t b, int64_t e) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * AR_THREADS;
+  for (int64_t i = b + static_cast<int64_t>(blockIdx.x) * AR_THREADS + threadIdx.x; i < e;
+       i += stride) {
+    const float4 v = reinterpret_cast<const float4*>(local)[i];
+    asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(mc + 4 * i),
+                 "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+                 : "memory");
+  }
+}
+
+__global__ void __launch_bounds__(AR_THREADS)
+k_p2p_bcast_f32(PeerPtrs peers, int rank, int world, int64_t b, int64_t e) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * AR_THREADS;
+  for (int64_t i = b + static_cast<int64_t>(blockIdx.x) * AR_THREADS + threadIdx.x; i < e;
+       i += stride) {
+    const float4 v = reinterpret_cast<const float4*>(peers.p[rank])[i];
+    for (int q = 0; q < world; ++q)
+      if (q != rank) reinterpret_cast<float4*>(peers.p[q])[i] = v;
+  }
+}
+
 __global__ void __launch_bounds__(256)
 k_f32_rows_to_bf16(const float* __restrict__ src, int64_t R, int h, __nv_bfloat16* dst,
                    int64_t ld) {
@@ -99,6 +123,36 @@ rl_status rl_allreduce_sum_f32(float* const* peer_ptrs, float* mc_ptr, int32_t r
       pp.p[q] = peer_ptrs[q];
     }
     k_p2p_allreduce_f32<<<blocks, AR_THREADS, 0, s>>>(pp, n4, rank, world);
+  }
+  RLH_CHECK_LAUNCH();
+  return RL_OK;
+}
+
+rl_status rl_allgather_rows_f32(float* const* peer_ptrs, float* mc_ptr, int32_t rank,
+                                int32_t world, int64_t num_rows, int64_t cols,
+                                int64_t rows_per_rank, rl_stream_t stream) {
+  if (world < 1 || world > AR_MAX_PEERS || rank < 0 || rank >= world || num_rows < 0 ||
+      cols <= 0 || (cols & 3) || rows_per_rank <= 0 || !peer_ptrs)
+    return RL_ERR_INVALID_ARG;
+  if (world == 1 || num_rows == 0) return RL_OK;
+  PeerPtrs pp{};
+  for (int q = 0; q < world; ++q) {
+    if (!peer_ptrs[q] || (reinterpret_cast<uintptr_t>(peer_ptrs[q]) & 15) != 0)
+      return RL_ERR_INVALID_ARG;
+    pp.p[q] = peer_ptrs[q];
+  }
+  const int64_t r0 = std::min<int64_t>(static_cast<int64_t>(rank) * rows_per_rank, num_rows);
+  const int64_t r1 = rank == world - 1 ? num_rows : std::min(r0 + rows_per_rank, num_rows);
+  if (r1 <= r0) return RL_OK;
+  const int64_t b = r0 * cols / 4, e = r1 * cols / 4;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(e - b, AR_THREADS), 148 * 4));
+  TraceScope ts(RL_K_MISC, s);
+  if (mc_ptr) {
+    if ((reinterpret_cast<uintptr_t>(mc_ptr) & 15) != 0) return RL_ERR_INVALID_ARG;
+    k_nvls_bcast_f32<<<blocks, AR_THREADS, 0, s>>>(pp.p[rank], mc_ptr, b, e);
+  } else {
+    k_p2p_bcast_f32<<<blocks, AR_THREADS, 0, s>>>(pp, rank, world, b, e);
   }
   RLH_CHECK_LAUNCH();
   return RL_OK;

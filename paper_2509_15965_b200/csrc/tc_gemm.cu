@@ -99,6 +99,13 @@ struct TcArgs {
   // EPI_ACC
   float* acc;
   int64_t ld_acc;
+  // EPI_ACC reduce-scatter (DP dW, last micro-batch): row j
+  // belongs to rank min(j / rs_rows, rs_world - 1); the epilogue adds
+  // (local partial + tile) into the owner's buffer with red.add over NVLink.
+  int32_t rs_world;    // 0 = off
+  int32_t rs_rank;
+  int64_t rs_rows;
+  float* rs_peer[8];
 };
 
 __device__ __forceinline__ void tile_coords(int64_t tile, int64_t m_tiles, int n_tiles,
@@ -117,13 +124,16 @@ __device__ __forceinline__ void tile_coords(int64_t tile, int64_t m_tiles, int n
 struct Prob {
   int64_t M = 0, num_k = 0, m_tiles = 0, tiles = 0;
   int32_t n_tiles = 1, group_m = 1;
-  __device__ void init(int64_t M_, int64_t K_, int tile_m, int32_t n_tiles_, int32_t group_m_) {
+  // keep_empty: run the epilogue even when K == 0 (its accumulator reads as
+  // 0) -- the dW reduce-scatter must still send this rank's partial.
+  __device__ void init(int64_t M_, int64_t K_, int tile_m, int32_t n_tiles_, int32_t group_m_,
+                       bool keep_empty = false) {
     M = M_;
     m_tiles = (M_ + tile_m - 1) / tile_m;
     num_k = (K_ + TC_BK - 1) / TC_BK;
     n_tiles = n_tiles_;
     group_m = group_m_;
-    tiles = num_k > 0 ? m_tiles * n_tiles_ : 0;
+    tiles = (num_k > 0 || keep_empty) ? m_tiles * n_tiles_ : 0;
   }
 };
 
@@ -184,10 +194,11 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   // wave of one fills with tiles of the other.
   const int64_t T = args.hdr->n_active;
   Prob P0, P1;
-  P0.init(args.m_dyn ? T : args.M, args.k_dyn ? T : args.K, C::TILE_M, args.n_tiles, args.group_m);
+  P0.init(args.m_dyn ? T : args.M, args.k_dyn ? T : args.K, C::TILE_M, args.n_tiles, args.group_m,
+          EPI == EPI_ACC && args.rs_world > 0);
   if constexpr (EPI == EPI_BWD)
     P1.init(args.m_dyn2 ? T : args.M2, args.k_dyn2 ? T : args.K2, C::TILE_M, args.n_tiles2,
-            args.group_m2);
+            args.group_m2, args.rs_world > 0);
   const int64_t num_tiles = P0.tiles + P1.tiles;
   const int64_t cid = blockIdx.x / CG, ncl = gridDim.x / CG;
   // per tile: which problem, its coordinates and K extent
@@ -472,21 +483,47 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         }
       } else {  // EPI_ACC (or the dW half of EPI_BWD)
         float4* dst = reinterpret_cast<float4*>(args.acc + row * args.ld_acc + n0);
+        const bool empty_k = P.num_k == 0;  // keep_empty tile: no MMA ran
 #pragma unroll 1
         for (int c = 0; c < C::TILE_N / 32; ++c) {
           uint32_t v[32];
           tmem_ld_32x32b_x32(taddr + c * 32, v);
           tmem_ld_wait();
           if (c == C::TILE_N / 32 - 1) release(acc);
-          if (row_ok && n0 + c * 32 < args.N) {
+          if (empty_k) {
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              float4 o = dst[c * 8 + q];
-              o.x += __uint_as_float(v[4 * q]);
-              o.y += __uint_as_float(v[4 * q + 1]);
-              o.z += __uint_as_float(v[4 * q + 2]);
-              o.w += __uint_as_float(v[4 * q + 3]);
-              dst[c * 8 + q] = o;
+            for (int j = 0; j < 32; ++j) v[j] = 0u;
+          }
+          if (row_ok && n0 + c * 32 < args.N) {
+            if (args.rs_world > 0) {
+              int64_t own = row / args.rs_rows;
+              own = own < args.rs_world - 1 ? own : args.rs_world - 1;
+              float* peer = args.rs_peer[own] + row * args.ld_acc + n0 + c * 32;
+              if (own == args.rs_rank) {  // other ranks add into these rows too
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                  red_add_v4_f32(peer + 4 * q, v[4 * q], v[4 * q + 1], v[4 * q + 2],
+                                 v[4 * q + 3]);
+              } else {  // send local partial + tile to the owner
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                  const float4 o = dst[c * 8 + q];
+                  red_add_v4_f32(peer + 4 * q, __float_as_uint(o.x + __uint_as_float(v[4 * q])),
+                                 __float_as_uint(o.y + __uint_as_float(v[4 * q + 1])),
+                                 __float_as_uint(o.z + __uint_as_float(v[4 * q + 2])),
+                                 __float_as_uint(o.w + __uint_as_float(v[4 * q + 3])));
+                }
+              }
+            } else {
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                float4 o = dst[c * 8 + q];
+                o.x += __uint_as_float(v[4 * q]);
+                o.y += __uint_as_float(v[4 * q + 1]);
+                o.z += __uint_as_float(v[4 * q + 2]);
+                o.w += __uint_as_float(v[4 * q + 3]);
+                dst[c * 8 + q] = o;
+              }
             }
           }
         }
@@ -680,7 +717,8 @@ rl_status launch_tc_fwd(const rl_head* hd, const void* weight, const WsLayout& L
 
 rl_status launch_tc_bwd(const rl_head* hd, const void* weight, void* grad_hidden,
                         float* grad_hidden_f32, bool gh_multicast, float* grad_weight,
-                        bool entropy_on, const WsLayout& L, char* ws, cudaStream_t s) {
+                        const rl_peer_group* dw_rs, bool entropy_on, const WsLayout& L, char* ws,
+                        cudaStream_t s) {
   const int h = hd->hidden, V = hd->vocab;
   const int cg = tc_cta_group();
   __nv_bfloat16* dz = reinterpret_cast<__nv_bfloat16*>(ws + L.off_dz);
@@ -732,6 +770,12 @@ rl_status launch_tc_bwd(const rl_head* hd, const void* weight, void* grad_hidden
   t7.N = h;
   t7.acc = grad_weight;
   t7.ld_acc = h;
+  if (dw_rs && dw_rs->world > 1) {
+    t7.rs_world = dw_rs->world;
+    t7.rs_rank = dw_rs->rank;
+    t7.rs_rows = dw_rs->rows_per_rank;
+    for (int q = 0; q < dw_rs->world; ++q) t7.rs_peer[q] = dw_rs->peers[q];
+  }
   if (fused_bwd()) {
     // one persistent launch over the dH tiles then the dW tiles: the last
     // (partial) wave of dH fills with dW tiles instead of idling.
@@ -745,6 +789,10 @@ rl_status launch_tc_bwd(const rl_head* hd, const void* weight, void* grad_hidden
     t.group_m2 = t.group_m;
     t.acc = grad_weight;
     t.ld_acc = h;
+    t.rs_world = t7.rs_world;
+    t.rs_rank = t7.rs_rank;
+    t.rs_rows = t7.rs_rows;
+    for (int q = 0; q < 8; ++q) t.rs_peer[q] = t7.rs_peer[q];
     const int64_t tiles = (ceil_div(L.Rp, 2 * TC_BM) + ceil_div(V, 2 * TC_BM)) * t.n_tiles;
     return run_gemm<2, 2, 0, 1, EPI_BWD>(ma6, mb6, ma7, mb7, t, tiles, RL_K_GEMM_DHDW, s);
   }

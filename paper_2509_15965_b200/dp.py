@@ -15,7 +15,10 @@
   a DDP-style mean would be off by world_size), stats all-reduce.
 
 Collectives go through torch.distributed (NCCL over NVLink on the B200 box,
-gloo on CPU in the tests); nothing else crosses ranks.
+gloo on CPU in the tests); nothing else crosses ranks. ``collective="symm"``
+replaces the dW all-reduce (the one exchange that follows a GEMM) by the
+reduce-scatter fused into the last micro-batch's dW GEMM epilogue plus an
+NVLink all-gather over torch symmetric memory.
 """
 from __future__ import annotations
 
@@ -73,6 +76,13 @@ def shard_layout(layout, rank: int, world: int):
 
 
 # ------------------------------------------------------------ collectives ----
+def _world(group=None) -> int:
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_world_size(group)
+    return 1
+
+
 def all_reduce_(t, op="sum", group=None):
     import torch.distributed as dist
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
@@ -133,10 +143,16 @@ def device_batch(layout, mb_rows: int, device="cuda") -> DeviceBatch:
 class PolicyLossStep:
     """One GRPO mini-batch step of the head on this rank."""
 
-    def __init__(self, head, weight, db: DeviceBatch, params=None, group=None):
+    def __init__(self, head, weight, db: DeviceBatch, params=None, group=None,
+                 advantage: str = "grpo", collective: str = "nccl"):
         import torch
         from . import rlhead as R
         self.R = R
+        if advantage not in ("grpo", "reinforce_pp"):
+            raise ValueError(f"unknown advantage {advantage!r}")
+        if collective not in ("nccl", "symm"):
+            raise ValueError(f"unknown collective {collective!r}")
+        self.advantage = advantage
         self.head, self.W, self.db = head, weight, db
         self.params = params or R.LossParams()
         self.group = group
@@ -146,7 +162,23 @@ class PolicyLossStep:
         self.params.n_tokens_global = self.n_global
         self.params.n_seqs_global = self.n_seqs
         self.adv = torch.empty(max(db.cu.shape[0] - 1, 1), dtype=torch.float32, device=dev)
-        self.grad_w = torch.zeros(weight.shape[0], weight.shape[1], dtype=torch.float32, device=dev)
+        self.symm = None
+        if collective == "symm" and _world(group) > 1:
+            # C3 over NVLink peer memory: grad_w in symmetric
+            # memory; the last micro-batch's dW epilogue reduce-scatters into
+            # the owners' slabs, rl_allgather_rows_f32 broadcasts them.
+            import torch.distributed as dist
+            import torch.distributed._symmetric_memory as symm_mem
+            V, h = weight.shape
+            t = symm_mem.empty(V * h, dtype=torch.float32, device=dev)
+            hdl = symm_mem.rendezvous(t, group if group is not None else dist.group.WORLD)
+            self.grad_w = t.view(V, h)
+            rows = -(-V // hdl.world_size)
+            self.peer_group = R.PeerGroup(hdl.rank, hdl.world_size, rows, list(hdl.buffer_ptrs))
+            self.symm = hdl
+        else:
+            self.grad_w = torch.zeros(weight.shape[0], weight.shape[1], dtype=torch.float32,
+                                      device=dev)
         self.stats = R.new_stats(dev)
         self.logp = torch.empty(max(db.num_rows, 1), dtype=torch.float32, device=dev)
         self.ws = R.Workspace(dev)
@@ -164,7 +196,25 @@ class PolicyLossStep:
         all_reduce_(self.n_seqs, "sum", self.group)
 
     def advantages(self):
-        self.R.rl_grpo_advantage(self.db.rewards, self.db.gos, self.db.num_groups, self.adv)
+        """GRPO (groups are rank-local under LPT sharding) or the REINFORCE++
+        batch normalisation, whose 5 batch statistics span all ranks (C2')."""
+        R, db = self.R, self.db
+        if self.advantage == "grpo":
+            R.rl_grpo_advantage(db.rewards, db.gos, db.num_groups, self.adv)
+            return
+        import torch
+        dev = self.adv.device
+        G = max(db.num_groups, 1)
+        gsum = torch.empty(G, 3, dtype=torch.float64, device=dev)
+        gmax = torch.empty(G, 2, dtype=torch.float64, device=dev)
+        R.rl_grpo_group_stats(db.rewards, db.gos, db.num_groups, gsum, gmax)
+        bst = torch.empty(5, dtype=torch.float64, device=dev)
+        R.rl_batch_norm_advantage(db.rewards, db.gos, db.num_groups, None, group_baseline=True,
+                                  group_sum_stats=gsum, batch_stats_out=bst)
+        all_reduce_(bst[:3], "sum", self.group)
+        all_reduce_(bst[3:], "max", self.group)
+        R.rl_batch_norm_advantage(db.rewards, db.gos, db.num_groups, self.adv,
+                                  group_baseline=True, group_sum_stats=gsum, batch_stats_in=bst)
 
     def run(self, hidden, old_logp, grad_hidden, hidden_for_mb=None, after_mb=None):
         """hidden [R, h] (or ``hidden_for_mb(i)`` -> the micro-batch's rows, for
@@ -172,21 +222,34 @@ class PolicyLossStep:
         largest micro-batch (its rows then hold the last micro-batch's dH,
         which the trunk backward would consume before the next one)."""
         R = self.R
+        self.grad_w.zero_()
+        if self.symm is not None:
+            self.symm.barrier(channel=0)   # every buffer zeroed before any rank adds into it
         self.count_tokens()
         self.advantages()
-        self.grad_w.zero_()
         self.stats.zero_()
         full_gh = grad_hidden.shape[0] >= self.db.num_rows
+        last = len(self.db.mbs) - 1
         for i, (s0, s1, r0, r1, cu_mb) in enumerate(self.db.mbs):
             hs = hidden_for_mb(i) if hidden_for_mb else hidden[r0:r1]
             gh = grad_hidden[r0:r1] if full_gh else grad_hidden[:r1 - r0]
             b = R.Batch(cu_mb, self.db.targets[r0:r1], self.db.mask[r0:r1], num_rows=r1 - r0)
+            self.params.dw_reduce_scatter = (self.peer_group if self.symm is not None and i == last
+                                             else None)
             R.rl_policy_loss_fwd_bwd(self.head, hs, self.W, b, old_logp[r0:r1], self.adv[s0:s1],
                                      self.params, self.logp[r0:r1], gh,
                                      self.grad_w, stats=self.stats, ws=self.ws)
             if after_mb:
                 after_mb(i)
-        all_reduce_(self.grad_w, "sum", self.group)
+        self.params.dw_reduce_scatter = None
+        if self.symm is not None:
+            hdl, pg = self.symm, self.peer_group
+            hdl.barrier(channel=0)         # every rank's adds into the owned slabs landed
+            R.rl_allgather_rows_f32(self.grad_w, pg.rank, pg.world, pg.rows_per_rank,
+                                    pg.peers, mc_ptr=hdl.multicast_ptr)
+            hdl.barrier(channel=0)         # every slab broadcast
+        else:
+            all_reduce_(self.grad_w, "sum", self.group)
         reduce_stats_(self.stats, self.group)
         return self.stats
 
@@ -222,7 +285,23 @@ class StreamingPolicyLoss:
         self.max_ratio, self.max_mean_ratio = max_ratio, max_mean_ratio
         self.n_tokens = torch.zeros(1, dtype=torch.int64, device=dev)
         self.stop_flag = torch.zeros(1, dtype=torch.int32, device=dev)
-        self.grad_w = torch.zeros(weight.shape[0], weight.shape[1], dtype=torch.float32, device=dev)
+        self.symm = None
+        if collective == "symm" and _world(group) > 1:
+            # C3 over NVLink peer memory: grad_w in symmetric
+            # memory; the last micro-batch's dW epilogue reduce-scatters into
+            # the owners' slabs, rl_allgather_rows_f32 broadcasts them.
+            import torch.distributed as dist
+            import torch.distributed._symmetric_memory as symm_mem
+            V, h = weight.shape
+            t = symm_mem.empty(V * h, dtype=torch.float32, device=dev)
+            hdl = symm_mem.rendezvous(t, group if group is not None else dist.group.WORLD)
+            self.grad_w = t.view(V, h)
+            rows = -(-V // hdl.world_size)
+            self.peer_group = R.PeerGroup(hdl.rank, hdl.world_size, rows, list(hdl.buffer_ptrs))
+            self.symm = hdl
+        else:
+            self.grad_w = torch.zeros(weight.shape[0], weight.shape[1], dtype=torch.float32,
+                                      device=dev)
         self.stats = R.new_stats(dev)
         self.ws = R.Workspace(dev)
         self.ws_prep = R.Workspace(dev)

@@ -40,12 +40,17 @@ class rl_head(C.Structure):
                 ("vocab_offset", C.c_int64), ("vocab_total", C.c_int64)]
 
 
+class rl_peer_group(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("world", C.c_int32), ("rows_per_rank", C.c_int64),
+                ("peers", C.c_void_p * 8)]
+
+
 class rl_loss_params(C.Structure):
     _fields_ = [("clip_lo", C.c_float), ("clip_hi", C.c_float), ("logratio_clamp", C.c_float),
                 ("loss_scale", C.c_double), ("n_tokens_global", C.c_void_p),
                 ("dual_clip", C.c_float), ("kl_coef", C.c_float), ("entropy_coef", C.c_float),
                 ("seq_mean", C.c_int32), ("ref_logp", C.c_void_p), ("n_seqs_global", C.c_void_p),
-                ("adv_per_token", C.c_int32)]
+                ("adv_per_token", C.c_int32), ("dw_reduce_scatter", C.POINTER(rl_peer_group))]
 
 
 class rl_value_params(C.Structure):
@@ -75,6 +80,11 @@ lib.rl_grpo_group_stats.argtypes = [_vp, _vp, C.c_int32, C.c_int32, _vp, _vp, _v
 lib.rl_grpo_advantage.restype = C.c_int
 lib.rl_grpo_advantage.argtypes = [_vp, _vp, C.c_int32, C.c_int32, _vp, _vp, C.c_float, C.c_int32,
                                   _vp, _vp, _vp]
+lib.rl_batch_norm_advantage.restype = C.c_int
+lib.rl_batch_norm_advantage.argtypes = [_vp, _vp, C.c_int32, C.c_int32, C.c_int32, _vp, _vp, _vp,
+                                        C.c_float, C.c_int32, _vp, _vp, _vp]
+lib.rl_read_device_error.restype = C.c_int
+lib.rl_read_device_error.argtypes = [_vp, C.POINTER(C.c_int32), _vp]
 lib.rl_policy_loss_fwd_bwd.restype = C.c_int
 lib.rl_policy_loss_fwd_bwd.argtypes = [C.POINTER(rl_head), _vp, _vp, C.POINTER(rl_batch), _vp,
                                        _vp, C.POINTER(rl_loss_params), _vp, _vp, _vp, _vp, _vp,
@@ -92,6 +102,9 @@ lib.rl_policy_loss_fwd_bwd_vp.argtypes = [C.POINTER(rl_head), _vp, _vp, C.POINTE
 lib.rl_allreduce_sum_f32.restype = C.c_int
 lib.rl_allreduce_sum_f32.argtypes = [C.POINTER(C.c_void_p), _vp, C.c_int32, C.c_int32, C.c_int64,
                                      _vp]
+lib.rl_allgather_rows_f32.restype = C.c_int
+lib.rl_allgather_rows_f32.argtypes = [C.POINTER(C.c_void_p), _vp, C.c_int32, C.c_int32,
+                                      C.c_int64, C.c_int64, C.c_int64, _vp]
 lib.rl_cast_rows_bf16.restype = C.c_int
 lib.rl_cast_rows_bf16.argtypes = [_vp, C.c_int64, C.c_int32, _vp, C.c_int64, _vp]
 lib.rl_minibatch_early_stop.restype = C.c_int
@@ -123,7 +136,8 @@ EXPORTED = ["rl_workspace_size", "rl_batch_prepare", "rl_logprob_fwd", "rl_grpo_
             "rl_logprob_partials", "rl_logprob_merge", "rl_policy_loss_fwd_bwd_vp",
             "rl_minibatch_early_stop", "rl_scale_by_inverse_count", "rl_gae",
             "rl_value_workspace_size", "rl_value_loss_fwd_bwd", "rl_allreduce_sum_f32",
-            "rl_cast_rows_bf16"]
+            "rl_cast_rows_bf16", "rl_batch_norm_advantage", "rl_read_device_error",
+            "rl_allgather_rows_f32"]
 
 
 class RLHeadError(RuntimeError):
@@ -196,12 +210,31 @@ class LossParams:
     ref_logp: object = None         # device fp32 [R] (needed when kl_coef > 0)
     n_seqs_global: object = None    # device int64[1]: S for seq_mean
     adv_per_token: bool = False     # adv [R] per row (PPO/GAE) instead of [S]
+    dw_reduce_scatter: object = None  # PeerGroup: fused DP dW reduce-scatter (last micro-batch)
 
     def c(self) -> rl_loss_params:
-        return rl_loss_params(self.clip_lo, self.clip_hi, self.logratio_clamp, self.loss_scale,
-                              _ptr(self.n_tokens_global), self.dual_clip, self.kl_coef,
-                              self.entropy_coef, int(bool(self.seq_mean)), _ptr(self.ref_logp),
-                              _ptr(self.n_seqs_global), int(bool(self.adv_per_token)))
+        pg = self.dw_reduce_scatter.c() if self.dw_reduce_scatter is not None else None
+        p = rl_loss_params(self.clip_lo, self.clip_hi, self.logratio_clamp, self.loss_scale,
+                           _ptr(self.n_tokens_global), self.dual_clip, self.kl_coef,
+                           self.entropy_coef, int(bool(self.seq_mean)), _ptr(self.ref_logp),
+                           _ptr(self.n_seqs_global), int(bool(self.adv_per_token)),
+                           C.pointer(pg) if pg is not None else None)
+        p._keep = pg                # keep the pointed-to struct alive with the params
+        return p
+
+
+@dataclass
+class PeerGroup:
+    """rl_peer_group: every rank's grad_weight (symmetric memory) and the
+    row-slab ownership of the fused dW reduce-scatter (include/rlhead.h)."""
+    rank: int
+    world: int
+    rows_per_rank: int
+    peers: list                     # device addresses (ints), peers[rank] = own buffer
+
+    def c(self) -> rl_peer_group:
+        arr = (C.c_void_p * 8)(*([int(x) for x in self.peers] + [0] * (8 - len(self.peers))))
+        return rl_peer_group(int(self.rank), int(self.world), int(self.rows_per_rank), arr)
 
 
 class Workspace:
@@ -273,6 +306,36 @@ def rl_grpo_advantage(rewards, group_of_seq, num_groups: int, adv, sum_stats=Non
                                  int(num_groups), _ptr(sum_stats), _ptr(max_stats), float(eps),
                                  int(bool(unbiased)), _ptr(adv), _ptr(err_flags),
                                  _stream(stream)), "rl_grpo_advantage")
+
+
+def rl_batch_norm_advantage(rewards, group_of_seq, num_groups: int, adv, group_baseline=True,
+                            group_sum_stats=None, batch_stats_in=None, batch_stats_out=None,
+                            eps: float = 1e-6, unbiased: bool = True, err_flags=None,
+                            stream=None):
+    """REINFORCE++-style batch-normalised advantage (NEXT-1). With the group
+    baseline and no group_sum_stats given, the group sums are computed here
+    (rl_grpo_group_stats into a scratch tensor) -- all members local."""
+    import torch
+    if group_baseline and group_sum_stats is None:
+        G = max(int(num_groups), 1)
+        group_sum_stats = torch.empty(G, 3, dtype=torch.float64, device=rewards.device)
+        mx = torch.empty(G, 2, dtype=torch.float64, device=rewards.device)
+        rl_grpo_group_stats(rewards, group_of_seq, num_groups, group_sum_stats, mx,
+                            err_flags=err_flags, stream=stream)
+    _check(lib.rl_batch_norm_advantage(_ptr(rewards), _ptr(group_of_seq), int(rewards.shape[0]),
+                                       int(num_groups), int(bool(group_baseline)),
+                                       _ptr(group_sum_stats), _ptr(batch_stats_in),
+                                       _ptr(batch_stats_out), float(eps), int(bool(unbiased)),
+                                       _ptr(adv), _ptr(err_flags), _stream(stream)),
+           "rl_batch_norm_advantage")
+
+
+def rl_read_device_error(err_flags, stream=None) -> int:
+    """Debug helper: synchronise the stream and return the device error word."""
+    v = C.c_int32(0)
+    _check(lib.rl_read_device_error(_ptr(err_flags), C.byref(v), _stream(stream)),
+           "rl_read_device_error")
+    return int(v.value)
 
 
 def rl_policy_loss_fwd_bwd(head: Head, hidden, weight, batch: Batch, old_logp, adv,
@@ -349,6 +412,17 @@ def rl_allreduce_sum_f32(buf, rank: int, world: int, peer_ptrs=None, mc_ptr: int
         arr = (C.c_void_p * world)(*[int(x) for x in peer_ptrs])
     _check(lib.rl_allreduce_sum_f32(arr, C.c_void_p(int(mc_ptr)) if mc_ptr else None, int(rank),
                                     int(world), n, _stream(stream)), "rl_allreduce_sum_f32")
+
+
+def rl_allgather_rows_f32(buf, rank: int, world: int, rows_per_rank: int, peer_ptrs,
+                          mc_ptr: int = 0, stream=None):
+    """Broadcast this rank's owned row slab of buf [rows, cols] fp32 to every
+    rank (multicast when mc_ptr != 0, else P2P stores to peer_ptrs)."""
+    rows, cols = buf.shape
+    arr = (C.c_void_p * world)(*[int(x) for x in peer_ptrs])
+    _check(lib.rl_allgather_rows_f32(arr, C.c_void_p(int(mc_ptr)) if mc_ptr else None, int(rank),
+                                     int(world), int(rows), int(cols), int(rows_per_rank),
+                                     _stream(stream)), "rl_allgather_rows_f32")
 
 
 def rl_cast_rows_bf16(src, dst, stream=None):

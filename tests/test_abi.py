@@ -60,7 +60,8 @@ def test_struct_layouts_match_header(tmp_path):
     if not shutil.which("gcc"):
         pytest.skip("gcc not available")
     structs = {"rl_batch": R.rl_batch, "rl_head": R.rl_head, "rl_loss_params": R.rl_loss_params,
-               "rl_loss_stats": R.rl_loss_stats}
+               "rl_loss_stats": R.rl_loss_stats, "rl_peer_group": R.rl_peer_group,
+               "rl_value_params": R.rl_value_params}
     lines = ["#include <stdio.h>", "#include <stddef.h>", f'#include "{HEADER}"', "int main(){"]
     for s, cls in structs.items():
         lines.append(f'printf("{s} %zu\\n", sizeof({s}));')

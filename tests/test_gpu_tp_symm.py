@@ -33,3 +33,24 @@ def test_tp2_all_collectives():
         assert r["max_dlogp"] <= 2e-3, (mode, r)
         assert r["rel_dH"] <= 1e-2 and r["rel_dW"] <= 1e-2, (mode, r)
         assert r["ranks_identical_dH"], (mode, r)
+
+
+@pytest.mark.parametrize("empty_last", [False, True])
+def test_dp2_fused_dw_reduce_scatter(empty_last):
+    """the DP step with the dW reduce-scatter fused into the
+    last micro-batch's dW GEMM epilogue + NVLink all-gather gives the NCCL
+    all-reduce's dW (fp32 atomics reorder the adds: rel 1e-6) on every rank,
+    also when one rank's last micro-batch has no active row (K = 0)."""
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29534",
+           os.path.join(ROOT, "scripts", "dp_check.py"), "--config", "qwen1.5b", "--max-mb", "2",
+           "--mb-rows", "8192", "--reps", "1"] + (["--empty-last"] if empty_last else [])
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-3000:]
+    res = json.loads([x for x in out.stdout.splitlines() if x.startswith("{")][-1])
+    assert res["norm_dW"] > 0 and res["rel_dW_symm_vs_nccl"] <= 1e-5, res
+    assert res["tokens"] == res["tokens_symm"]
+    assert all(m["ranks_identical_dW"] for m in res["modes"].values()), res

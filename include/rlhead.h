@@ -194,30 +194,30 @@ typedef struct {
                                      per row (PPO/GAE, NEXT-4)                        */
   const struct rl_peer_group *dw_reduce_scatter; /* NULL: grad_weight += locally.
                                      Else (the LAST micro-batch of a mini-batch on
-                                     every DP rank; bf16 tensor-core path): see
-                                     rl_peer_group                                     */
+                                     every DP rank; bf16 tensor-core path): partial +
+                                     this micro-batch go to the owners' staging
+                                     buffers instead, see rl_peer_group                */
 } rl_loss_params;
 
 /* DP reduction of dW fused into the last micro-batch's dW GEMM (C3 of
- * SURVEY §8(e)). grad_weight [V][h] fp32 (ld = h) lives in
- * memory every rank of the group has mapped (symmetric memory); rows are
- * owned in slabs: owner(j) = min(j / rows_per_rank, world - 1). With
- * params->dw_reduce_scatter set, the dW epilogue adds, for every finished
- * tile, (this rank's accumulated partial + the tile) into the OWNER's
- * grad_weight with red.add over NVLink (the owner adds its own tile in
- * place), so the reduce-scatter overlaps the GEMM tile by tile. After the
- * call returned on every rank and a cross-rank barrier, rows owned by rank
- * r hold the SUM over ranks in rank r's buffer (fp32 atomics: the order of
- * the adds is not fixed); the other rows of a buffer keep that rank's local
- * partial. rl_allgather_rows_f32 then broadcasts each slab (all-reduce).
- * The caller zeroes every rank's grad_weight and barriers before any rank
- * starts that mini-batch's last micro-batch. */
+ * SURVEY §8(e)). Vocab rows are owned in slabs:
+ * owner(j) = min(j / rows_per_rank, world - 1), rows_per_rank * world >= V.
+ * Every rank has a staging buffer float [world][rows_per_rank][h] that all
+ * ranks have mapped (symmetric memory; peers[q] = rank q's). With
+ * params->dw_reduce_scatter set, the dW epilogue stores, for every finished
+ * tile, (this rank's accumulated grad_weight partial + the tile) into slot
+ * [rank][j - owner*rows_per_rank] of the OWNER's staging buffer over NVLink
+ * (plain stores; a rank whose micro-batch has no active row still sends its
+ * partial), so the reduce-scatter runs tile by tile under the GEMM. The
+ * local grad_weight is read, not updated. After the call returned on every
+ * rank and a cross-rank barrier, rl_reduce_bcast_rows_f32 on every rank sums
+ * its slab's `world` slots in rank order (deterministic) and broadcasts the
+ * sum into every rank's dW buffer (all-reduce). bf16 tensor-core path only. */
 typedef struct rl_peer_group {
   int32_t rank;                   /* this rank in the group                          */
   int32_t world;                  /* 1..8                                            */
-  int64_t rows_per_rank;          /* > 0                                             */
-  float *peers[8];                /* device: every rank's grad_weight, peers[rank]
-                                     == this call's grad_weight                      */
+  int64_t rows_per_rank;          /* > 0, rows_per_rank * world >= vocab             */
+  float *peers[8];                /* device: every rank's staging buffer             */
 } rl_peer_group;
 
 /* Loss statistics, device resident, ACCUMULATED (+=) by every call. The
@@ -363,15 +363,19 @@ RL_API rl_status rl_policy_loss_fwd_bwd_vp(const rl_head *hd, const void *hidden
  * 1 <= world <= 8, else RL_ERR_INVALID_ARG; world == 1 is a no-op. */
 RL_API rl_status rl_allreduce_sum_f32(float *const *peer_ptrs, float *mc_ptr, int32_t rank,
                                       int32_t world, int64_t n, rl_stream_t stream);
-/* All-gather of row slabs over NVLink peer memory: rank `rank` broadcasts
- * its owned rows [rank*rows_per_rank, min((rank+1)*rows_per_rank, num_rows))
- * (the last rank owns through num_rows) of buf [num_rows][cols] fp32 to
- * every rank's buf -- multimem.st through the multicast address mc_ptr when
- * given, else plain stores to peer_ptrs (HOST array of world device
- * pointers). Bracket with cross-rank barriers. cols % 4 == 0. */
-RL_API rl_status rl_allgather_rows_f32(float *const *peer_ptrs, float *mc_ptr, int32_t rank,
-                                       int32_t world, int64_t num_rows, int64_t cols,
-                                       int64_t rows_per_rank, rl_stream_t stream);
+/* Owner side of the fused DP dW reduce-scatter (rl_peer_group): rank `rank`
+ * owns rows [rank*rows_per_rank, min((rank+1)*rows_per_rank, num_rows)) of
+ * the [num_rows][cols] fp32 dW; out[row] = sum over q = 0..world-1 (in this
+ * order) of staging[q][row - rank*rows_per_rank] (staging = this rank's
+ * [world][rows_per_rank][cols] buffer), stored into EVERY rank's output --
+ * multimem.st through the multicast address out_mc when given, else plain
+ * stores to out_peers (HOST array of world device pointers). Bracket with
+ * cross-rank barriers. cols % 4 == 0, 16-B aligned pointers. */
+RL_API rl_status rl_reduce_bcast_rows_f32(const float *staging, float *const *out_peers,
+                                          float *out_mc, int32_t rank, int32_t world,
+                                          int64_t num_rows, int64_t cols, int64_t rows_per_rank,
+                                          rl_stream_t stream);
+
 /* dst[t][0:hidden] (bf16, row stride ld) = round-to-nearest(src[t][0:hidden])
  * (fp32, row stride hidden), t < num_rows; hidden even, ld >= hidden even. */
 RL_API rl_status rl_cast_rows_bf16(const float *src, int64_t num_rows, int32_t hidden, void *dst,

@@ -320,7 +320,7 @@ static rl_status loss_impl(const rl_head* hd, const void* hidden, const void* we
   const rl_peer_group* rs = p->dw_reduce_scatter;
   if (rs) {
     if (rs->world < 1 || rs->world > 8 || rs->rank < 0 || rs->rank >= rs->world ||
-        rs->rows_per_rank <= 0 || rs->peers[rs->rank] != grad_weight)
+        rs->rows_per_rank <= 0 || rs->rows_per_rank * rs->world < hd->vocab)
       return RL_ERR_INVALID_ARG;
     for (int q = 0; q < rs->world; ++q)
       if (!rs->peers[q] || !aligned(rs->peers[q], 16)) return RL_ERR_INVALID_ARG;

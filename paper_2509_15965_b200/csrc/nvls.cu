@@ -1,6 +1,7 @@
 // Collectives over NVLink peer memory for the two exchange steps that follow
-// a GEMM on the hot path: the DP sum of dW and the
-// vocab-parallel sum of dL/dH. The GEMM epilogue writes its fp32 result
+// a GEMM on the hot path: the vocab-parallel sum of
+// dL/dH (below) and the owner side of the DP dW reduce-scatter
+// (k_reduce_bcast_f32; the send side is the dW GEMM epilogue). The GEMM epilogue writes its fp32 result
 // straight into a symmetric buffer (mapped on every rank); after a cross-rank
 // barrier this kernel sums the P copies without NCCL and without staging:
 //  * NVLS (NVLink SHARP, multicast object available): two-shot all-reduce --
@@ -61,27 +62,33 @@ k_p2p_allreduce_f32(PeerPtrs peers, int64_t n4, int rank, int world) {
   }
 }
 
-// All-gather of this rank's slab [b, e) (float4 units): multicast or P2P.
+// Owner side of the DP dW reduce-scatter: sum the `world`
+// staged copies of this rank's slab in rank order (deterministic) and store
+// the sum into every rank's output -- multimem.st through the multicast
+// address, or plain stores to each peer. i: float4 index within the slab.
 __global__ void __launch_bounds__(AR_THREADS)
-k_nvls_bcast_f32(const float* __restrict__ local, float* mc, int64_t b, int64_t e) {
+k_reduce_bcast_f32(const float* __restrict__ staging, int64_t slab4, int world, PeerPtrs out,
+                   float* mc, int64_t off4, int64_t n4) {
   const int64_t stride = static_cast<int64_t>(gridDim.x) * AR_THREADS;
-  for (int64_t i = b + static_cast<int64_t>(blockIdx.x) * AR_THREADS + threadIdx.x; i < e;
+  const float4* st = reinterpret_cast<const float4*>(staging);
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * AR_THREADS + threadIdx.x; i < n4;
        i += stride) {
-    const float4 v = reinterpret_cast<const float4*>(local)[i];
-    asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(mc + 4 * i),
-                 "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
-                 : "memory");
-  }
-}
-
-__global__ void __launch_bounds__(AR_THREADS)
-k_p2p_bcast_f32(PeerPtrs peers, int rank, int world, int64_t b, int64_t e) {
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * AR_THREADS;
-  for (int64_t i = b + static_cast<int64_t>(blockIdx.x) * AR_THREADS + threadIdx.x; i < e;
-       i += stride) {
-    const float4 v = reinterpret_cast<const float4*>(peers.p[rank])[i];
-    for (int q = 0; q < world; ++q)
-      if (q != rank) reinterpret_cast<float4*>(peers.p[q])[i] = v;
+    float4 s = st[i];
+    for (int q = 1; q < world; ++q) {
+      const float4 v = st[q * slab4 + i];
+      s.x += v.x;
+      s.y += v.y;
+      s.z += v.z;
+      s.w += v.w;
+    }
+    if (mc) {
+      asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(
+                       mc + 4 * (off4 + i)),
+                   "f"(s.x), "f"(s.y), "f"(s.z), "f"(s.w)
+                   : "memory");
+    } else {
+      for (int q = 0; q < world; ++q) reinterpret_cast<float4*>(out.p[q])[off4 + i] = s;
+    }
   }
 }
 
@@ -128,32 +135,33 @@ rl_status rl_allreduce_sum_f32(float* const* peer_ptrs, float* mc_ptr, int32_t r
   return RL_OK;
 }
 
-rl_status rl_allgather_rows_f32(float* const* peer_ptrs, float* mc_ptr, int32_t rank,
-                                int32_t world, int64_t num_rows, int64_t cols,
-                                int64_t rows_per_rank, rl_stream_t stream) {
+rl_status rl_reduce_bcast_rows_f32(const float* staging, float* const* out_peers, float* out_mc,
+                                   int32_t rank, int32_t world, int64_t num_rows, int64_t cols,
+                                   int64_t rows_per_rank, rl_stream_t stream) {
   if (world < 1 || world > AR_MAX_PEERS || rank < 0 || rank >= world || num_rows < 0 ||
-      cols <= 0 || (cols & 3) || rows_per_rank <= 0 || !peer_ptrs)
+      cols <= 0 || (cols & 3) || rows_per_rank <= 0 || rows_per_rank * world < num_rows ||
+      !staging || (reinterpret_cast<uintptr_t>(staging) & 15) != 0)
     return RL_ERR_INVALID_ARG;
-  if (world == 1 || num_rows == 0) return RL_OK;
   PeerPtrs pp{};
-  for (int q = 0; q < world; ++q) {
-    if (!peer_ptrs[q] || (reinterpret_cast<uintptr_t>(peer_ptrs[q]) & 15) != 0)
-      return RL_ERR_INVALID_ARG;
-    pp.p[q] = peer_ptrs[q];
+  if (!out_mc) {
+    if (!out_peers) return RL_ERR_INVALID_ARG;
+    for (int q = 0; q < world; ++q) {
+      if (!out_peers[q] || (reinterpret_cast<uintptr_t>(out_peers[q]) & 15) != 0)
+        return RL_ERR_INVALID_ARG;
+      pp.p[q] = out_peers[q];
+    }
+  } else if ((reinterpret_cast<uintptr_t>(out_mc) & 15) != 0) {
+    return RL_ERR_INVALID_ARG;
   }
   const int64_t r0 = std::min<int64_t>(static_cast<int64_t>(rank) * rows_per_rank, num_rows);
-  const int64_t r1 = rank == world - 1 ? num_rows : std::min(r0 + rows_per_rank, num_rows);
+  const int64_t r1 = std::min(r0 + rows_per_rank, num_rows);
   if (r1 <= r0) return RL_OK;
-  const int64_t b = r0 * cols / 4, e = r1 * cols / 4;
+  const int64_t n4 = (r1 - r0) * cols / 4;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(e - b, AR_THREADS), 148 * 4));
+  const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(n4, AR_THREADS), 148 * 4));
   TraceScope ts(RL_K_MISC, s);
-  if (mc_ptr) {
-    if ((reinterpret_cast<uintptr_t>(mc_ptr) & 15) != 0) return RL_ERR_INVALID_ARG;
-    k_nvls_bcast_f32<<<blocks, AR_THREADS, 0, s>>>(pp.p[rank], mc_ptr, b, e);
-  } else {
-    k_p2p_bcast_f32<<<blocks, AR_THREADS, 0, s>>>(pp, rank, world, b, e);
-  }
+  k_reduce_bcast_f32<<<blocks, AR_THREADS, 0, s>>>(staging, rows_per_rank * cols / 4, world, pp,
+                                                   out_mc, r0 * cols / 4, n4);
   RLH_CHECK_LAUNCH();
   return RL_OK;
 }

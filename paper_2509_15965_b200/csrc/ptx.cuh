@@ -171,14 +171,6 @@ __device__ __forceinline__ void multimem_red_add_v4_f32(void* mc, uint32_t a, ui
                : "memory");
 }
 
-// Atomic add of four fp32 to a (local or NVLink-peer) global address.
-__device__ __forceinline__ void red_add_v4_f32(void* p, uint32_t a, uint32_t b, uint32_t c,
-                                               uint32_t d) {
-  asm volatile("red.relaxed.sys.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(a),
-               "r"(b), "r"(c), "r"(d)
-               : "memory");
-}
-
 // ------------------------------------------------- clusters / CTA pairs ----
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;

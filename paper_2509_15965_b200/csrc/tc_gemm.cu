@@ -100,12 +100,14 @@ struct TcArgs {
   float* acc;
   int64_t ld_acc;
   // EPI_ACC reduce-scatter (DP dW, last micro-batch): row j
-  // belongs to rank min(j / rs_rows, rs_world - 1); the epilogue adds
-  // (local partial + tile) into the owner's buffer with red.add over NVLink.
+  // belongs to rank o = min(j / rs_rows, rs_world - 1); the epilogue stores
+  // (local partial + tile) into slot [rs_rank][j - o rs_rows] of the owner's
+  // staging buffer over NVLink (plain stores; the owner sums the slots in
+  // rank order afterwards, so the result is deterministic).
   int32_t rs_world;    // 0 = off
   int32_t rs_rank;
   int64_t rs_rows;
-  float* rs_peer[8];
+  float* rs_peer[8];   // every rank's staging buffer [rs_world][rs_rows][ld_acc]
 };
 
 __device__ __forceinline__ void tile_coords(int64_t tile, int64_t m_tiles, int n_tiles,
@@ -495,24 +497,21 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             for (int j = 0; j < 32; ++j) v[j] = 0u;
           }
           if (row_ok && n0 + c * 32 < args.N) {
-            if (args.rs_world > 0) {
+            if (args.rs_world > 0) {  // local partial + tile -> the owner's slot
               int64_t own = row / args.rs_rows;
               own = own < args.rs_world - 1 ? own : args.rs_world - 1;
-              float* peer = args.rs_peer[own] + row * args.ld_acc + n0 + c * 32;
-              if (own == args.rs_rank) {  // other ranks add into these rows too
+              float4* slot = reinterpret_cast<float4*>(
+                  args.rs_peer[own] +
+                  (args.rs_rank * args.rs_rows + (row - own * args.rs_rows)) * args.ld_acc + n0 +
+                  c * 32);
 #pragma unroll
-                for (int q = 0; q < 8; ++q)
-                  red_add_v4_f32(peer + 4 * q, v[4 * q], v[4 * q + 1], v[4 * q + 2],
-                                 v[4 * q + 3]);
-              } else {  // send local partial + tile to the owner
-#pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                  const float4 o = dst[c * 8 + q];
-                  red_add_v4_f32(peer + 4 * q, __float_as_uint(o.x + __uint_as_float(v[4 * q])),
-                                 __float_as_uint(o.y + __uint_as_float(v[4 * q + 1])),
-                                 __float_as_uint(o.z + __uint_as_float(v[4 * q + 2])),
-                                 __float_as_uint(o.w + __uint_as_float(v[4 * q + 3])));
-                }
+              for (int q = 0; q < 8; ++q) {
+                float4 o = dst[c * 8 + q];
+                o.x += __uint_as_float(v[4 * q]);
+                o.y += __uint_as_float(v[4 * q + 1]);
+                o.z += __uint_as_float(v[4 * q + 2]);
+                o.w += __uint_as_float(v[4 * q + 3]);
+                slot[q] = o;
               }
             } else {
 #pragma unroll

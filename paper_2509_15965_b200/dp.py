@@ -164,17 +164,23 @@ class PolicyLossStep:
         self.adv = torch.empty(max(db.cu.shape[0] - 1, 1), dtype=torch.float32, device=dev)
         self.symm = None
         if collective == "symm" and _world(group) > 1:
-            # C3 over NVLink peer memory: grad_w in symmetric
-            # memory; the last micro-batch's dW epilogue reduce-scatters into
-            # the owners' slabs, rl_allgather_rows_f32 broadcasts them.
+            # C3 over NVLink peer memory: the last micro-batch's
+            # dW epilogue stores (partial + tile) into the owners' staging slots;
+            # rl_reduce_bcast_rows_f32 sums them in rank order and broadcasts.
             import torch.distributed as dist
             import torch.distributed._symmetric_memory as symm_mem
             V, h = weight.shape
+            grp = group if group is not None else dist.group.WORLD
+            P = _world(group)
+            rows = -(-V // P)
             t = symm_mem.empty(V * h, dtype=torch.float32, device=dev)
-            hdl = symm_mem.rendezvous(t, group if group is not None else dist.group.WORLD)
+            hdl = symm_mem.rendezvous(t, grp)
+            stg = symm_mem.empty(P * rows * h, dtype=torch.float32, device=dev)
+            hdl_s = symm_mem.rendezvous(stg, grp)
             self.grad_w = t.view(V, h)
-            rows = -(-V // hdl.world_size)
-            self.peer_group = R.PeerGroup(hdl.rank, hdl.world_size, rows, list(hdl.buffer_ptrs))
+            self.staging = stg
+            self.peer_group = R.PeerGroup(hdl.rank, P, rows, list(hdl_s.buffer_ptrs))
+            self.out_peers = list(hdl.buffer_ptrs)
             self.symm = hdl
         else:
             self.grad_w = torch.zeros(weight.shape[0], weight.shape[1], dtype=torch.float32,
@@ -223,8 +229,6 @@ class PolicyLossStep:
         which the trunk backward would consume before the next one)."""
         R = self.R
         self.grad_w.zero_()
-        if self.symm is not None:
-            self.symm.barrier(channel=0)   # every buffer zeroed before any rank adds into it
         self.count_tokens()
         self.advantages()
         self.stats.zero_()
@@ -244,9 +248,10 @@ class PolicyLossStep:
         self.params.dw_reduce_scatter = None
         if self.symm is not None:
             hdl, pg = self.symm, self.peer_group
-            hdl.barrier(channel=0)         # every rank's adds into the owned slabs landed
-            R.rl_allgather_rows_f32(self.grad_w, pg.rank, pg.world, pg.rows_per_rank,
-                                    pg.peers, mc_ptr=hdl.multicast_ptr)
+            hdl.barrier(channel=0)         # every rank's slots in every staging buffer written
+            R.rl_reduce_bcast_rows_f32(self.staging, self.grad_w, pg.rank, pg.world,
+                                       pg.rows_per_rank, self.out_peers,
+                                       mc_ptr=hdl.multicast_ptr)
             hdl.barrier(channel=0)         # every slab broadcast
         else:
             all_reduce_(self.grad_w, "sum", self.group)
@@ -285,23 +290,8 @@ class StreamingPolicyLoss:
         self.max_ratio, self.max_mean_ratio = max_ratio, max_mean_ratio
         self.n_tokens = torch.zeros(1, dtype=torch.int64, device=dev)
         self.stop_flag = torch.zeros(1, dtype=torch.int32, device=dev)
-        self.symm = None
-        if collective == "symm" and _world(group) > 1:
-            # C3 over NVLink peer memory: grad_w in symmetric
-            # memory; the last micro-batch's dW epilogue reduce-scatters into
-            # the owners' slabs, rl_allgather_rows_f32 broadcasts them.
-            import torch.distributed as dist
-            import torch.distributed._symmetric_memory as symm_mem
-            V, h = weight.shape
-            t = symm_mem.empty(V * h, dtype=torch.float32, device=dev)
-            hdl = symm_mem.rendezvous(t, group if group is not None else dist.group.WORLD)
-            self.grad_w = t.view(V, h)
-            rows = -(-V // hdl.world_size)
-            self.peer_group = R.PeerGroup(hdl.rank, hdl.world_size, rows, list(hdl.buffer_ptrs))
-            self.symm = hdl
-        else:
-            self.grad_w = torch.zeros(weight.shape[0], weight.shape[1], dtype=torch.float32,
-                                      device=dev)
+        self.grad_w = torch.zeros(weight.shape[0], weight.shape[1], dtype=torch.float32,
+                                  device=dev)
         self.stats = R.new_stats(dev)
         self.ws = R.Workspace(dev)
         self.ws_prep = R.Workspace(dev)

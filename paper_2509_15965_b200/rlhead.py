@@ -102,9 +102,9 @@ lib.rl_policy_loss_fwd_bwd_vp.argtypes = [C.POINTER(rl_head), _vp, _vp, C.POINTE
 lib.rl_allreduce_sum_f32.restype = C.c_int
 lib.rl_allreduce_sum_f32.argtypes = [C.POINTER(C.c_void_p), _vp, C.c_int32, C.c_int32, C.c_int64,
                                      _vp]
-lib.rl_allgather_rows_f32.restype = C.c_int
-lib.rl_allgather_rows_f32.argtypes = [C.POINTER(C.c_void_p), _vp, C.c_int32, C.c_int32,
-                                      C.c_int64, C.c_int64, C.c_int64, _vp]
+lib.rl_reduce_bcast_rows_f32.restype = C.c_int
+lib.rl_reduce_bcast_rows_f32.argtypes = [_vp, C.POINTER(C.c_void_p), _vp, C.c_int32, C.c_int32,
+                                         C.c_int64, C.c_int64, C.c_int64, _vp]
 lib.rl_cast_rows_bf16.restype = C.c_int
 lib.rl_cast_rows_bf16.argtypes = [_vp, C.c_int64, C.c_int32, _vp, C.c_int64, _vp]
 lib.rl_minibatch_early_stop.restype = C.c_int
@@ -137,7 +137,7 @@ EXPORTED = ["rl_workspace_size", "rl_batch_prepare", "rl_logprob_fwd", "rl_grpo_
             "rl_minibatch_early_stop", "rl_scale_by_inverse_count", "rl_gae",
             "rl_value_workspace_size", "rl_value_loss_fwd_bwd", "rl_allreduce_sum_f32",
             "rl_cast_rows_bf16", "rl_batch_norm_advantage", "rl_read_device_error",
-            "rl_allgather_rows_f32"]
+            "rl_reduce_bcast_rows_f32"]
 
 
 class RLHeadError(RuntimeError):
@@ -225,12 +225,13 @@ class LossParams:
 
 @dataclass
 class PeerGroup:
-    """rl_peer_group: every rank's grad_weight (symmetric memory) and the
-    row-slab ownership of the fused dW reduce-scatter (include/rlhead.h)."""
+    """rl_peer_group: every rank's dW staging buffer [world, rows_per_rank, h]
+    (symmetric memory) and the row-slab ownership of the fused dW
+    reduce-scatter (include/rlhead.h)."""
     rank: int
     world: int
     rows_per_rank: int
-    peers: list                     # device addresses (ints), peers[rank] = own buffer
+    peers: list                     # device addresses (ints) of every rank's staging buffer
 
     def c(self) -> rl_peer_group:
         arr = (C.c_void_p * 8)(*([int(x) for x in self.peers] + [0] * (8 - len(self.peers))))
@@ -414,15 +415,20 @@ def rl_allreduce_sum_f32(buf, rank: int, world: int, peer_ptrs=None, mc_ptr: int
                                     int(world), n, _stream(stream)), "rl_allreduce_sum_f32")
 
 
-def rl_allgather_rows_f32(buf, rank: int, world: int, rows_per_rank: int, peer_ptrs,
-                          mc_ptr: int = 0, stream=None):
-    """Broadcast this rank's owned row slab of buf [rows, cols] fp32 to every
-    rank (multicast when mc_ptr != 0, else P2P stores to peer_ptrs)."""
-    rows, cols = buf.shape
-    arr = (C.c_void_p * world)(*[int(x) for x in peer_ptrs])
-    _check(lib.rl_allgather_rows_f32(arr, C.c_void_p(int(mc_ptr)) if mc_ptr else None, int(rank),
-                                     int(world), int(rows), int(cols), int(rows_per_rank),
-                                     _stream(stream)), "rl_allgather_rows_f32")
+def rl_reduce_bcast_rows_f32(staging, out, rank: int, world: int, rows_per_rank: int,
+                             out_peer_ptrs=None, mc_ptr: int = 0, stream=None):
+    """Owner side of the fused DP dW reduce-scatter: sum this rank's `world`
+    staged slab copies (staging [world, rows_per_rank, cols]) in rank order and
+    store the sum into every rank's out [rows, cols] (multicast when mc_ptr,
+    else P2P stores to out_peer_ptrs)."""
+    rows, cols = out.shape
+    arr = None
+    if not mc_ptr:
+        arr = (C.c_void_p * world)(*[int(x) for x in out_peer_ptrs])
+    _check(lib.rl_reduce_bcast_rows_f32(_ptr(staging), arr,
+                                        C.c_void_p(int(mc_ptr)) if mc_ptr else None, int(rank),
+                                        int(world), int(rows), int(cols), int(rows_per_rank),
+                                        _stream(stream)), "rl_reduce_bcast_rows_f32")
 
 
 def rl_cast_rows_bf16(src, dst, stream=None):

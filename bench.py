@@ -252,12 +252,13 @@ def main():
     clk.start()
     tr = rl.Trace(1 << 17).start()
     n0 = rl.rl_launch_count()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    e0, e1 = evs[0], evs[-1]
     barrier()
     e0.record()
-    for _ in range(args.steps):
+    for i in range(args.steps):
         step.run(H, old, gh)
-    e1.record()
+        evs[i + 1].record()
     barrier()
     launches = rl.rl_launch_count() - n0
     tr.stop()
@@ -267,6 +268,7 @@ def main():
         dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     ms_per_step = float(ms.item())
     value = tokens_global / (ms_per_step / 1e3)
+    per_step = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]   # this rank
 
     # roofline of the dominant kernel (GEMM kinds: 2hV flops per token per launch)
     pk = peaks()
@@ -316,6 +318,8 @@ def main():
             "metric": METRIC, "value": round(value, 1), "unit": "tokens/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "step_ms_rank0": {"median": round(statistics.median(per_step), 3),
+                              "min": round(min(per_step), 3), "max": round(max(per_step), 3)},
             "data": "synthetic",
             "config": {"workload": f"{cfg.name} head (h={cfg.hidden}, V={cfg.vocab}), "
                                    f"{cfg.prompts} prompts x G={cfg.group}, responses <= {cfg.lmax}",

@@ -61,13 +61,18 @@ def pack_micro_batches(seq_rows, budget: int):
     return out
 
 
-def shard_layout(layout, rank: int, world: int):
-    """This rank's sequences (whole groups, LPT by response tokens)."""
+def shard_layout(layout, rank: int, world: int, split_groups: bool = False):
+    """This rank's sequences, LPT by response tokens: whole groups (advantages
+    rank-local), or with ``split_groups`` single sequences (finer balance; the
+    group statistics are then all-reduced)."""
     G = layout.num_groups
     cu = layout.cu_seqlens.astype(np.int64)
     seq_tokens = np.add.reduceat(layout.mask.astype(np.int64), cu[:-1]) \
         if layout.num_rows else np.zeros(layout.num_seqs, np.int64)
     seq_tokens = np.where(cu[1:] > cu[:-1], seq_tokens, 0)
+    if split_groups:
+        bins, loads = lpt_shard(seq_tokens, world)
+        return list(bins[rank]), loads
     g_tokens = np.bincount(layout.group_of_seq, weights=seq_tokens, minlength=G).astype(np.int64)
     bins, loads = lpt_shard(g_tokens, world)
     mine = set(bins[rank])
@@ -119,12 +124,17 @@ class DeviceBatch:
     seq_rows: np.ndarray = field(default=None)
 
 
-def device_batch(layout, mb_rows: int, device="cuda") -> DeviceBatch:
+def device_batch(layout, mb_rows: int, device="cuda", global_groups: bool = False) -> DeviceBatch:
+    """global_groups: keep the mini-batch-wide group ids (split-group mode, whose
+    group statistics are all-reduced by id); else local ids 0..G'-1."""
     import torch
     cu_np = layout.cu_seqlens.astype(np.int64)
     seq_rows = cu_np[1:] - cu_np[:-1]
-    # local group ids 0..G'-1 (keeps the GRPO launch small)
-    uniq, gos_local = np.unique(layout.group_of_seq, return_inverse=True)
+    if global_groups:
+        uniq = np.arange(layout.num_groups)
+        gos_local = np.asarray(layout.group_of_seq)
+    else:  # local group ids 0..G'-1 (keeps the GRPO launch small)
+        uniq, gos_local = np.unique(layout.group_of_seq, return_inverse=True)
     mbs = []
     for s0, s1 in pack_micro_batches(seq_rows, mb_rows):
         r0, r1 = int(cu_np[s0]), int(cu_np[s1])
@@ -144,7 +154,7 @@ class PolicyLossStep:
     """One GRPO mini-batch step of the head on this rank."""
 
     def __init__(self, head, weight, db: DeviceBatch, params=None, group=None,
-                 advantage: str = "grpo", collective: str = "nccl"):
+                 advantage: str = "grpo", collective: str = "nccl", split_groups: bool = False):
         import torch
         from . import rlhead as R
         self.R = R
@@ -153,6 +163,7 @@ class PolicyLossStep:
         if collective not in ("nccl", "symm"):
             raise ValueError(f"unknown collective {collective!r}")
         self.advantage = advantage
+        self.split_groups = split_groups
         self.head, self.W, self.db = head, weight, db
         self.params = params or R.LossParams()
         self.group = group
@@ -205,7 +216,7 @@ class PolicyLossStep:
         """GRPO (groups are rank-local under LPT sharding) or the REINFORCE++
         batch normalisation, whose 5 batch statistics span all ranks (C2')."""
         R, db = self.R, self.db
-        if self.advantage == "grpo":
+        if self.advantage == "grpo" and not self.split_groups:
             R.rl_grpo_advantage(db.rewards, db.gos, db.num_groups, self.adv)
             return
         import torch
@@ -214,6 +225,13 @@ class PolicyLossStep:
         gsum = torch.empty(G, 3, dtype=torch.float64, device=dev)
         gmax = torch.empty(G, 2, dtype=torch.float64, device=dev)
         R.rl_grpo_group_stats(db.rewards, db.gos, db.num_groups, gsum, gmax)
+        if self.split_groups:          # C2: a group's members may sit on several ranks
+            all_reduce_(gsum, "sum", self.group)
+            all_reduce_(gmax, "max", self.group)
+        if self.advantage == "grpo":
+            R.rl_grpo_advantage(db.rewards, db.gos, db.num_groups, self.adv, sum_stats=gsum,
+                                max_stats=gmax)
+            return
         bst = torch.empty(5, dtype=torch.float64, device=dev)
         R.rl_batch_norm_advantage(db.rewards, db.gos, db.num_groups, None, group_baseline=True,
                                   group_sum_stats=gsum, batch_stats_out=bst)

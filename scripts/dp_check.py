@@ -24,6 +24,9 @@ def main():
     ap.add_argument("--max-mb", type=int, default=3)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--empty-last", action="store_true")
+    ap.add_argument("--modes", default="nccl,symm",
+                    help="comma list of nccl|symm[-split]; -split = sequence-level sharding "
+                         "with all-reduced group statistics (compare with --max-mb 0)")
     a = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -38,31 +41,46 @@ def main():
     dist.init_process_group("nccl", device_id=dev)
     cfg = CONFIGS[a.config]
     layout = make_layout(cfg, 0)
-    seqs, _ = shard_layout(layout, rank, world)
-    mine, _ = sub_layout(layout, seqs)
-    if a.empty_last and rank == 1:
-        db0 = device_batch(mine, a.mb_rows, device=dev)
-        n = min(len(db0.mbs), a.max_mb)
-        _, _, r0, r1, _ = db0.mbs[n - 1]
-        mine.mask[r0:r1] = 0
-    db = device_batch(mine, a.mb_rows, device=dev)
-    db.mbs = db.mbs[:a.max_mb]
     _, W = make_tensors_torch(cfg, 0, seed=1, device=dev, hidden=False)
-    H, _ = make_tensors_torch(cfg, mine.num_rows, seed=100 + rank, device=dev, weight=False)
     head = rl.Head(cfg.hidden, cfg.vocab, cfg.dtype)
-    # old log-probs = the policy's own (ratio 1): every unmasked token carries
-    # gradient (old = 0 would clamp d = logp - old and zero the gradients)
-    old = torch.zeros(max(mine.num_rows, 1), device=dev)
-    ws = rl.Workspace(dev)
-    for (_, _, r0, r1, cu_mb) in db.mbs:
-        rl.rl_logprob_fwd(head, H[r0:r1], W, rl.Batch(cu_mb, db.targets[r0:r1], db.mask[r0:r1],
-                                                      num_rows=r1 - r0), old[r0:r1], ws=ws)
-    del ws
-    gh = torch.empty(mine.num_rows, cfg.hidden, dtype=H.dtype, device=dev)
+    # hidden rows are a function of the GLOBAL row (seeded per sequence-independent
+    # chunks of the whole batch) so different shardings see the same data
+    Hg, _ = make_tensors_torch(cfg, layout.num_rows, seed=5, device=dev, weight=False)
+    cache = {}
+
+    def rank_data(split):
+        if split in cache:
+            return cache[split]
+        seqs, _ = shard_layout(layout, rank, world, split_groups=split)
+        mine, rows = sub_layout(layout, seqs)
+        if a.empty_last and rank == 1:
+            db0 = device_batch(mine, a.mb_rows, device=dev)
+            n = min(len(db0.mbs), a.max_mb) if a.max_mb else len(db0.mbs)
+            _, _, r0, r1, _ = db0.mbs[n - 1]
+            mine.mask[r0:r1] = 0
+        db = device_batch(mine, a.mb_rows, device=dev, global_groups=split)
+        if a.max_mb:
+            db.mbs = db.mbs[:a.max_mb]
+        H = Hg[torch.as_tensor(rows, device=dev)] if len(rows) else Hg[:1]
+        # old log-probs = the policy's own (ratio 1): every unmasked token carries
+        # gradient (old = 0 would clamp d = logp - old and zero the gradients)
+        old = torch.zeros(max(mine.num_rows, 1), device=dev)
+        ws = rl.Workspace(dev)
+        for (_, _, r0, r1, cu_mb) in db.mbs:
+            rl.rl_logprob_fwd(head, H[r0:r1], W, rl.Batch(cu_mb, db.targets[r0:r1],
+                                                          db.mask[r0:r1], num_rows=r1 - r0),
+                              old[r0:r1], ws=ws)
+        gh = torch.empty(max(mine.num_rows, 1), cfg.hidden, dtype=H.dtype, device=dev)
+        cache[split] = (db, H, old, gh)
+        return cache[split]
+
     out = {}
     res = {}
-    for mode in ("nccl", "symm"):
-        step = PolicyLossStep(head, W, db, collective=mode)
+    modes = a.modes.split(",")
+    for mode in modes:
+        split = mode.endswith("-split")
+        db, H, old, gh = rank_data(split)
+        step = PolicyLossStep(head, W, db, collective=mode.split("-")[0], split_groups=split)
         step.run(H, old, gh)
         torch.cuda.synchronize()
         dist.barrier()
@@ -79,17 +97,19 @@ def main():
         res[mode] = (step.grad_w.clone(), rl.read_stats(step.stats), gws)
         out[mode] = {"ms_per_step": round(float(ms.item()), 3),
                      "ranks_identical_dW": all(torch.equal(g, gws[0]) for g in gws)}
-    g_n, s_n, _ = res["nccl"]
-    g_s, s_s, _ = res["symm"]
+    g_n, s_n, _ = res[modes[0]]
     nrm = float(g_n.double().norm())
-    rel = float((g_s.double() - g_n.double()).norm()) / max(nrm, 1e-300)
+    for mode in modes[1:]:
+        g_s, s_s, _ = res[mode]
+        out[mode]["rel_dW_vs_" + modes[0]] = float((g_s.double() - g_n.double()).norm()) / max(
+            nrm, 1e-300)
+        out[mode]["tokens"] = s_s["tokens"]
+        out[mode]["loss_sum"] = s_s["loss_sum"]
+    out[modes[0]]["tokens"] = s_n["tokens"]
+    out[modes[0]]["loss_sum"] = s_n["loss_sum"]
     if rank == 0:
-        print(json.dumps({"world": world, "config": a.config, "micro_batches": len(db.mbs),
-                          "empty_last": a.empty_last, "rel_dW_symm_vs_nccl": rel,
-                          "norm_dW": nrm,
-                          "tokens": s_n["tokens"], "tokens_symm": s_s["tokens"],
-                          "loss_sum_nccl": s_n["loss_sum"], "loss_sum_symm": s_s["loss_sum"],
-                          "modes": out}), flush=True)
+        print(json.dumps({"world": world, "config": a.config, "empty_last": a.empty_last,
+                          "norm_dW": nrm, "modes": out}), flush=True)
     dist.destroy_process_group()
 
 

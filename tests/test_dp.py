@@ -131,3 +131,21 @@ def test_vocab_shards_cover_and_align(V, P):
     assert sh[0][0] == 0 and sum(s for _, s in sh) == V
     for (o1, s1), (o2, _) in zip(sh, sh[1:]):
         assert o2 == o1 + s1 and s1 % 256 == 0
+
+
+def test_shard_layout_split_groups_partition():
+    """Split-group sharding assigns single sequences by LPT: a partition of all
+    sequences, loads within one sequence's weight of each other."""
+    from paper_2509_15965_b200.dp import shard_layout
+    from workload import CONFIGS, make_layout
+    lay = make_layout(CONFIGS["qwen1.5b"], 0)
+    cu = lay.cu_seqlens.astype(np.int64)
+    tok = np.add.reduceat(lay.mask.astype(np.int64), cu[:-1])
+    for world in (2, 3, 8):
+        got = [shard_layout(lay, r, world, split_groups=True) for r in range(world)]
+        seqs = sorted(s for g, _ in got for s in g)
+        assert seqs == list(range(lay.num_seqs))
+        loads = got[0][1]
+        assert loads.max() - loads.min() <= tok.max()
+        for r, (g, _) in enumerate(got):
+            assert int(tok[g].sum()) == int(loads[r])

@@ -207,8 +207,10 @@ def main():
     seqs, loads = shard_layout(layout, rank, world)
     mine, _ = sub_layout(layout, seqs)
     db = device_batch(mine, args.mb_rows, device=dev)
-    if args.max_mb:
-        db.mbs = db.mbs[:args.max_mb]
+    if args.max_mb:  # debug: the sequences of the first max_mb micro-batches only
+        s_end = db.mbs[min(args.max_mb, len(db.mbs)) - 1][1]
+        mine, _ = sub_layout(mine, np.arange(s_end))
+        db = device_batch(mine, args.mb_rows, device=dev)
     _, W = make_tensors_torch(cfg, 0, seed=args.seed, device=dev, hidden=False)
     H, _ = make_tensors_torch(cfg, mine.num_rows, seed=args.seed + 7919 * (rank + 1), device=dev,
                               weight=False)

@@ -91,8 +91,10 @@ typedef struct {
   int64_t vocab_total;   /* full vocabulary (0 = unsharded)                    */
 } rl_head;
 
-/* Workspace bytes for a call on up to `num_rows` packed rows;
- * want_bwd != 0 for rl_policy_loss_fwd_bwd. 0 if the head is invalid. */
+/* Workspace bytes for a call on up to `num_rows` packed rows: want_bwd = 0
+ * for rl_logprob_fwd / the vocab-parallel calls, 1 for rl_policy_loss_fwd_bwd
+ * (+ _vp), 2 for rl_batch_prepare alone (bookkeeping only, ~21 B/row).
+ * 0 if the head or want_bwd is invalid. */
 RL_API size_t rl_workspace_size(const rl_head *hd, int64_t num_rows, int32_t want_bwd);
 
 /* H1 bookkeeping alone (it also runs inside the two head calls).

@@ -71,6 +71,7 @@ bool ws_layout(const rl_head* hd, int64_t R, int want_bwd, WsLayout* L) {
   L->off_rowseq = take(static_cast<size_t>(R) * 4);
   L->off_tgt = take(static_cast<size_t>(L->Rp) * 4);
   L->off_seq = take(static_cast<size_t>(L->Rp) * 4);
+  L->prep_total = o;  // everything rl_batch_prepare touches lies before this
   L->off_hc = take(tc ? static_cast<size_t>(L->Rp) * h * 2 : 0);
   L->off_pm = take(static_cast<size_t>(L->n_vt) * L->Rp * 4);
   L->off_ps = take(static_cast<size_t>(L->n_vt) * L->Rp * 4);
@@ -126,9 +127,10 @@ extern "C" {
 
 size_t rl_workspace_size(const rl_head* hd, int64_t num_rows, int32_t want_bwd) {
   if (!head_ok(hd) || num_rows < 0) return 0;
+  if (want_bwd < 0 || want_bwd > 2) return 0;
   WsLayout L;
-  ws_layout(hd, num_rows, want_bwd, &L);
-  return L.total;
+  ws_layout(hd, num_rows, want_bwd == 1, &L);
+  return want_bwd == 2 ? L.prep_total : L.total;
 }
 
 rl_status rl_batch_prepare(const rl_head* hd, const rl_batch* b, int32_t* row_seq,
@@ -137,7 +139,7 @@ rl_status rl_batch_prepare(const rl_head* hd, const rl_batch* b, int32_t* row_se
   if (!head_ok(hd) || !batch_ok(b)) return RL_ERR_INVALID_ARG;
   WsLayout L;
   ws_layout(hd, b->num_rows, 0, &L);
-  if (!ws || ws_bytes < L.total) return RL_ERR_WORKSPACE;
+  if (!ws || ws_bytes < L.prep_total) return RL_ERR_WORKSPACE;
   if (!aligned(ws, 256)) return RL_ERR_INVALID_ARG;
   return launch_prepare(hd, b, L, static_cast<char*>(ws), row_seq, active_idx, n_active, n_accum,
                         nseq_accum, nullptr, nullptr, nullptr,

@@ -49,6 +49,7 @@ struct WsLayout {
   int64_t Vp;             // vocab padded to TC_BN (dZ row stride)
   int64_t nblk_rows;      // 1024-row blocks of the bookkeeping kernels
   int64_t nblk_loss;      // 32-row blocks of the merge/loss kernel
+  size_t prep_total;      // bytes rl_batch_prepare needs (a prefix of the layout)
   size_t off_hdr, off_flags, off_blkcnt, off_blkoff, off_active, off_rowseq, off_tgt,
       off_seq, off_hc, off_pm, off_ps, off_pu, off_zy, off_lse, off_g, off_ge, off_ez, off_dz,
       off_st_d, off_st_f, off_st_i, total;

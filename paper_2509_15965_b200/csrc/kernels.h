@@ -31,7 +31,10 @@ rl_status launch_batch_adv(const float* rewards, const int32_t* gos, int32_t S, 
 
 // H4 merge of the split-V partials (+ H5 loss when old_logp != NULL).
 struct MergeArgs {
-  const float *pm, *ps, *pu, *zy;       // partial n of compact row r at [n * part_stride + r]
+  // partial n of compact row r: part_stride > 0: [n * part_stride + r] (the
+  // gathered vocab-parallel parts); part_stride == 0: this call's own split-V
+  // partials, row-blocked [((r >> 5) * nparts + n) * 32 + (r & 31)]
+  const float *pm, *ps, *pu, *zy;
   int64_t nparts, part_stride;
   const int32_t *active_idx, *seq_c;
   float *logp, *entropy, *lse;          // row space, may be NULL

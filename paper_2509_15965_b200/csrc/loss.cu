@@ -100,7 +100,7 @@ __device__ __forceinline__ void lse_fold(float& M, float& S, float& U, float m, 
 // (fixed, deterministic) and runs the per-row loss. 8x the loads in flight of
 // a thread-per-row loop, which left the kernel latency-bound.
 template <bool LOSS>
-__global__ void __launch_bounds__(MERGE_THREADS)
+__global__ void __launch_bounds__(MERGE_THREADS, 6)
 k_merge(MergeArgs a, const WsHeader* __restrict__ hdr, int64_t ldp) {
   __shared__ float sh_m[MERGE_SPLIT][MERGE_ROWS], sh_s[MERGE_SPLIT][MERGE_ROWS],
       sh_u[MERGE_SPLIT][MERGE_ROWS];
@@ -108,14 +108,45 @@ k_merge(MergeArgs a, const WsHeader* __restrict__ hdr, int64_t ldp) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t r = static_cast<int64_t>(blockIdx.x) * MERGE_ROWS + lane;
   const int64_t n_vt = a.nparts, pst = a.part_stride;
+  // element (n, r): strided [n * pst + r] or row-blocked [(rb * n_vt + n) * 32 + lane]
+  const int64_t base = pst ? r : (static_cast<int64_t>(blockIdx.x) * n_vt) * 32 + lane;
+  const int64_t nst = pst ? pst : 32;
   {
     float M = -INFINITY, S = 0.f, U = 0.f;
     if (r < T) {
       const int64_t per = (n_vt + MERGE_SPLIT - 1) / MERGE_SPLIT;
       const int64_t n0 = wid * per, n1 = n0 + per < n_vt ? n0 + per : n_vt;
-#pragma unroll 4
-      for (int64_t n = n0; n < n1; ++n)
-        lse_fold(M, S, U, a.pm[n * pst + r], a.ps[n * pst + r], a.pu[n * pst + r]);
+      int64_t n = n0;
+      // batches of 4 partials: 12 independent loads in flight, then one
+      // branch-free fold against the batch maximum (5 exps per 4 partials)
+      for (; n + 4 <= n1; n += 4) {
+        float m[4], sv[4], u[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int64_t o = base + (n + j) * nst;
+          m[j] = __ldcs(a.pm + o);
+          sv[j] = __ldcs(a.ps + o);
+          u[j] = __ldcs(a.pu + o);
+        }
+        const float Mn = fmaxf(fmaxf(fmaxf(m[0], m[1]), fmaxf(m[2], m[3])), M);
+        const bool empty = M == -INFINITY;
+        const float dM = empty ? 0.f : M - Mn;
+        const float f = empty ? 0.f : expf(dM);
+        float Sn = f * S, Un = f * (U + dM * S);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float d = m[j] - Mn, e = expf(d);
+          Sn += e * sv[j];
+          Un += e * (u[j] + d * sv[j]);
+        }
+        M = Mn;
+        S = Sn;
+        U = Un;
+      }
+      for (; n < n1; ++n) {
+        const int64_t o = base + n * nst;
+        lse_fold(M, S, U, a.pm[o], a.ps[o], a.pu[o]);
+      }
     }
     sh_m[wid][lane] = M;
     sh_s[wid][lane] = S;
@@ -230,9 +261,9 @@ rl_status launch_merge(const WsLayout& L, char* ws, const MergeArgs& a_in, cudaS
   const WsHeader* hdr = reinterpret_cast<const WsHeader*>(ws + L.off_hdr);
   if (L.nblk_loss == 0) return RL_OK;
   MergeArgs a = a_in;
-  if (a.nparts == 0) {  // this call's own split-V partials in the workspace
+  if (a.nparts == 0) {  // this call's own split-V partials in the workspace (row-blocked)
     a.nparts = L.n_vt;
-    a.part_stride = L.Rp;
+    a.part_stride = 0;
   }
   if (a.parts_out && a.old_logp) return RL_ERR_INVALID_ARG;
   TraceScope ts(RL_K_MERGE, s);

@@ -82,7 +82,7 @@ struct TcArgs {
   // EPI_LSE
   float *pm, *ps, *pu, *zy;
   const int32_t* tgt_c;
-  int64_t ldp;
+  int64_t ldp;         // (unused by the row-blocked partial layout)
   // EPI_DZ
   const float *lse_c, *g_c;
   const float *ge_c, *ez_c;  // entropy bonus (NULL = off): w c_ent and E_p[z]
@@ -396,7 +396,10 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         }
         release(acc);
         if (row_ok) {
-          const int64_t o = static_cast<int64_t>(nb) * args.ldp + row;
+          // row-blocked partials [Rp/32][n_vt][32]: a warp's 32 rows are 128 B
+          // per vocab tile here, and k_merge streams one row block's n_vt
+          // tiles contiguously
+          const int64_t o = ((row >> 5) * args.n_tiles + nb) * 32 + (row & 31);
           args.pm[o] = m;
           args.ps[o] = s;
           args.pu[o] = u;

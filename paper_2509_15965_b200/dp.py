@@ -88,6 +88,34 @@ def _world(group=None) -> int:
     return 1
 
 
+def _symm_dw_buffers(R, weight, group):
+    """C3 over NVLink peer memory: dW [V, h] and the staging
+    buffer [P, ceil(V/P), h] (fp32) in torch symmetric memory. The last
+    micro-batch's dW epilogue stores (partial + tile) into the owners' staging
+    slots; _symm_dw_finish sums them in rank order and broadcasts."""
+    import torch
+    import torch.distributed as dist
+    import torch.distributed._symmetric_memory as symm_mem
+    V, h = weight.shape
+    dev = weight.device
+    grp = group if group is not None else dist.group.WORLD
+    P = _world(group)
+    rows = -(-V // P)
+    t = symm_mem.empty(V * h, dtype=torch.float32, device=dev)
+    hdl = symm_mem.rendezvous(t, grp)
+    stg = symm_mem.empty(P * rows * h, dtype=torch.float32, device=dev)
+    hdl_s = symm_mem.rendezvous(stg, grp)
+    pg = R.PeerGroup(hdl.rank, P, rows, list(hdl_s.buffer_ptrs))
+    return t.view(V, h), stg, pg, list(hdl.buffer_ptrs), hdl
+
+
+def _symm_dw_finish(R, hdl, staging, grad_w, pg, out_peers):
+    hdl.barrier(channel=0)         # every rank's slots in every staging buffer written
+    R.rl_reduce_bcast_rows_f32(staging, grad_w, pg.rank, pg.world, pg.rows_per_rank, out_peers,
+                               mc_ptr=hdl.multicast_ptr)
+    hdl.barrier(channel=0)         # every slab broadcast
+
+
 def all_reduce_(t, op="sum", group=None):
     import torch.distributed as dist
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
@@ -175,24 +203,8 @@ class PolicyLossStep:
         self.adv = torch.empty(max(db.cu.shape[0] - 1, 1), dtype=torch.float32, device=dev)
         self.symm = None
         if collective == "symm" and _world(group) > 1:
-            # C3 over NVLink peer memory: the last micro-batch's
-            # dW epilogue stores (partial + tile) into the owners' staging slots;
-            # rl_reduce_bcast_rows_f32 sums them in rank order and broadcasts.
-            import torch.distributed as dist
-            import torch.distributed._symmetric_memory as symm_mem
-            V, h = weight.shape
-            grp = group if group is not None else dist.group.WORLD
-            P = _world(group)
-            rows = -(-V // P)
-            t = symm_mem.empty(V * h, dtype=torch.float32, device=dev)
-            hdl = symm_mem.rendezvous(t, grp)
-            stg = symm_mem.empty(P * rows * h, dtype=torch.float32, device=dev)
-            hdl_s = symm_mem.rendezvous(stg, grp)
-            self.grad_w = t.view(V, h)
-            self.staging = stg
-            self.peer_group = R.PeerGroup(hdl.rank, P, rows, list(hdl_s.buffer_ptrs))
-            self.out_peers = list(hdl.buffer_ptrs)
-            self.symm = hdl
+            self.grad_w, self.staging, self.peer_group, self.out_peers, self.symm = \
+                _symm_dw_buffers(R, weight, group)
         else:
             self.grad_w = torch.zeros(weight.shape[0], weight.shape[1], dtype=torch.float32,
                                       device=dev)
@@ -265,12 +277,8 @@ class PolicyLossStep:
                 after_mb(i)
         self.params.dw_reduce_scatter = None
         if self.symm is not None:
-            hdl, pg = self.symm, self.peer_group
-            hdl.barrier(channel=0)         # every rank's slots in every staging buffer written
-            R.rl_reduce_bcast_rows_f32(self.staging, self.grad_w, pg.rank, pg.world,
-                                       pg.rows_per_rank, self.out_peers,
-                                       mc_ptr=hdl.multicast_ptr)
-            hdl.barrier(channel=0)         # every slab broadcast
+            _symm_dw_finish(R, self.symm, self.staging, self.grad_w, self.peer_group,
+                            self.out_peers)
         else:
             all_reduce_(self.grad_w, "sum", self.group)
         reduce_stats_(self.stats, self.group)
@@ -294,7 +302,7 @@ class StreamingPolicyLoss:
     """
 
     def __init__(self, head, weight, params=None, group=None, max_ratio: float = 0.0,
-                 max_mean_ratio: float = 0.0):
+                 max_mean_ratio: float = 0.0, collective: str = "nccl"):
         import torch
         from . import rlhead as R
         self.R = R
@@ -308,8 +316,14 @@ class StreamingPolicyLoss:
         self.max_ratio, self.max_mean_ratio = max_ratio, max_mean_ratio
         self.n_tokens = torch.zeros(1, dtype=torch.int64, device=dev)
         self.stop_flag = torch.zeros(1, dtype=torch.int32, device=dev)
-        self.grad_w = torch.zeros(weight.shape[0], weight.shape[1], dtype=torch.float32,
-                                  device=dev)
+        self.symm = None
+        if collective == "symm" and _world(group) > 1:
+            self.grad_w, self.staging, self.peer_group, self.out_peers, self.symm = \
+                _symm_dw_buffers(R, weight, group)
+        else:
+            self.grad_w = torch.zeros(weight.shape[0], weight.shape[1], dtype=torch.float32,
+                                      device=dev)
+        self.sent = False
         self.stats = R.new_stats(dev)
         self.ws = R.Workspace(dev)
         self.ws_prep = R.Workspace(dev)
@@ -319,19 +333,52 @@ class StreamingPolicyLoss:
         self.stop_flag.zero_()
         self.grad_w.zero_()
         self.stats.zero_()
+        self.sent = False
 
-    def feed(self, hidden, batch, old_logp, adv, logp, grad_hidden, entropy=None):
+    def feed(self, hidden, batch, old_logp, adv, logp, grad_hidden, entropy=None,
+             last: bool = False):
+        """last=True on this rank's final micro-batch of the global batch lets its
+        dW epilogue run the fused reduce-scatter (collective="symm")."""
         R = self.R
         R.rl_batch_prepare(self.head, batch, n_accum=self.n_tokens, ws=self.ws_prep)
+        fuse = self.symm is not None and last and not self.sent
+        self.params.dw_reduce_scatter = self.peer_group if fuse else None
         R.rl_policy_loss_fwd_bwd(self.head, hidden, self.W, batch, old_logp, adv, self.params,
                                  logp, grad_hidden, self.grad_w, entropy=entropy,
                                  stats=self.stats, ws=self.ws)
+        self.params.dw_reduce_scatter = None
+        self.sent = self.sent or fuse
+
+    def _send_partial(self):
+        """No last=True feed on this rank: send the accumulated partial through a
+        one-row, fully masked micro-batch (its dW GEMM has K = 0 and only ships
+        the partial to the owners)."""
+        import torch
+        R, dev, h = self.R, self.grad_w.device, self.W.shape[1]
+        dt = self.W.dtype
+        b = R.Batch(torch.tensor([0, 1], dtype=torch.int32, device=dev),
+                    torch.zeros(1, dtype=torch.int32, device=dev),
+                    torch.zeros(1, dtype=torch.uint8, device=dev))
+        hid = torch.zeros(1, h, dtype=dt, device=dev)
+        one = torch.zeros(1, device=dev)
+        self.params.dw_reduce_scatter = self.peer_group
+        R.rl_policy_loss_fwd_bwd(self.head, hid, self.W, b, one, one, self.params,
+                                 torch.empty(1, device=dev), torch.empty_like(hid), self.grad_w,
+                                 ws=self.ws)
+        self.params.dw_reduce_scatter = None
+        self.sent = True
 
     def finish(self):
         R = self.R
         all_reduce_(self.n_tokens, "sum", self.group)
+        if self.symm is not None:
+            if not self.sent:
+                self._send_partial()
+            _symm_dw_finish(R, self.symm, self.staging, self.grad_w, self.peer_group,
+                            self.out_peers)
+        else:
+            all_reduce_(self.grad_w, "sum", self.group)
         R.rl_scale_by_inverse_count(self.grad_w, self.n_tokens)
-        all_reduce_(self.grad_w, "sum", self.group)
         reduce_stats_(self.stats, self.group)
         R.rl_minibatch_early_stop(self.stats, self.stop_flag, self.grad_w, self.max_ratio,
                                   self.max_mean_ratio)

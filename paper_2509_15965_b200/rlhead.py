@@ -265,9 +265,10 @@ def read_stats(t) -> dict:
 
 
 # --------------------------------------------------------------- C calls ----
-def rl_workspace_size(head: Head, num_rows: int, want_bwd: bool) -> int:
+def rl_workspace_size(head: Head, num_rows: int, want_bwd) -> int:
+    """want_bwd: False/0 forward, True/1 loss fwd+bwd, 2 rl_batch_prepare only."""
     hd = head.c()
-    n = lib.rl_workspace_size(C.byref(hd), int(num_rows), int(bool(want_bwd)))
+    n = lib.rl_workspace_size(C.byref(hd), int(num_rows), int(want_bwd))
     if n == 0:
         raise RLHeadError("rl_workspace_size: invalid head")
     return int(n)
@@ -277,7 +278,7 @@ def rl_batch_prepare(head: Head, batch: Batch, row_seq=None, active_idx=None, n_
                      n_accum=None, nseq_accum=None, ws: Workspace | None = None, stream=None):
     hd, b = head.c(), batch.c()
     ws = ws or Workspace()
-    nb = rl_workspace_size(head, b.num_rows, False)
+    nb = rl_workspace_size(head, b.num_rows, 2)      # bookkeeping-only prefix
     buf = ws.get(nb)
     _check(lib.rl_batch_prepare(C.byref(hd), C.byref(b), _ptr(row_seq), _ptr(active_idx),
                                 _ptr(n_active), _ptr(n_accum), _ptr(nseq_accum), _ptr(buf),

@@ -13,6 +13,8 @@ import json
 import os
 import sys
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
@@ -25,14 +27,17 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--empty-last", action="store_true")
     ap.add_argument("--modes", default="nccl,symm",
-                    help="comma list of nccl|symm[-split]; -split = sequence-level sharding "
-                         "with all-reduced group statistics (compare with --max-mb 0)")
+                    help="comma list of nccl|symm[-split] | stream-nccl|stream-symm[-nolast]; "
+                         "-split = sequence-level sharding with all-reduced group statistics "
+                         "(compare with --max-mb 0); stream-* = StreamingPolicyLoss (deferred "
+                         "1/N), -nolast = no last=True feed (partial sent by finish())")
     a = ap.parse_args()
     import torch
     import torch.distributed as dist
 
     import paper_2509_15965_b200 as rl
-    from paper_2509_15965_b200.dp import PolicyLossStep, device_batch, shard_layout
+    from paper_2509_15965_b200.dp import (PolicyLossStep, StreamingPolicyLoss, device_batch,
+                                          shard_layout)
     from workload import CONFIGS, make_layout, make_tensors_torch, sub_layout
     rank, world, local = (int(os.environ.get(k, d)) for k, d in
                           (("RANK", 0), ("WORLD_SIZE", 1), ("LOCAL_RANK", 0)))
@@ -58,9 +63,12 @@ def main():
             n = min(len(db0.mbs), a.max_mb) if a.max_mb else len(db0.mbs)
             _, _, r0, r1, _ = db0.mbs[n - 1]
             mine.mask[r0:r1] = 0
+        if a.max_mb:  # keep the sequences of the first max_mb micro-batches only
+            db0 = device_batch(mine, a.mb_rows, device=dev, global_groups=split)
+            s_end = db0.mbs[min(a.max_mb, len(db0.mbs)) - 1][1]
+            mine, sub_rows = sub_layout(mine, np.arange(s_end))
+            rows = rows[sub_rows]
         db = device_batch(mine, a.mb_rows, device=dev, global_groups=split)
-        if a.max_mb:
-            db.mbs = db.mbs[:a.max_mb]
         H = Hg[torch.as_tensor(rows, device=dev)] if len(rows) else Hg[:1]
         # old log-probs = the policy's own (ratio 1): every unmasked token carries
         # gradient (old = 0 would clamp d = logp - old and zero the gradients)
@@ -77,10 +85,35 @@ def main():
     out = {}
     res = {}
     modes = a.modes.split(",")
+
+    class Streamed:
+        """StreamingPolicyLoss driven like PolicyLossStep.run (stream-<coll>[-nolast])."""
+
+        def __init__(self, db, coll, use_last):
+            self.db, self.use_last = db, use_last
+            self.s = StreamingPolicyLoss(head, W, collective=coll)
+            self.adv = torch.empty(max(db.cu.shape[0] - 1, 1), device=dev)
+            self.logp = torch.empty(max(db.num_rows, 1), device=dev)
+            self.grad_w, self.stats = self.s.grad_w, self.s.stats
+
+        def run(self, H, old, gh):
+            db, st = self.db, self.s
+            rl.rl_grpo_advantage(db.rewards, db.gos, db.num_groups, self.adv)
+            st.begin()
+            for i, (s0, s1, r0, r1, cu_mb) in enumerate(db.mbs):
+                b = rl.Batch(cu_mb, db.targets[r0:r1], db.mask[r0:r1], num_rows=r1 - r0)
+                st.feed(H[r0:r1], b, old[r0:r1], self.adv[s0:s1], self.logp[r0:r1], gh[r0:r1],
+                        last=self.use_last and i == len(db.mbs) - 1)
+            st.finish()
+
     for mode in modes:
         split = mode.endswith("-split")
         db, H, old, gh = rank_data(split)
-        step = PolicyLossStep(head, W, db, collective=mode.split("-")[0], split_groups=split)
+        if mode.startswith("stream-"):
+            parts = mode.split("-")
+            step = Streamed(db, parts[1], "nolast" not in parts)
+        else:
+            step = PolicyLossStep(head, W, db, collective=mode.split("-")[0], split_groups=split)
         step.run(H, old, gh)
         torch.cuda.synchronize()
         dist.barrier()

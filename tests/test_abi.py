@@ -36,6 +36,10 @@ def test_workspace_size_and_validation_host_only():
     n_b = R.lib.rl_workspace_size(C.byref(hd), 65536, 1)
     # dZ chunk bf16 [Rp, Vp] dominates the backward workspace
     assert n_b - n_f >= 65536 * 152064 * 2
+    # bookkeeping-only prefix (rl_batch_prepare): ~21 B/row, independent of V and h
+    n_p = R.lib.rl_workspace_size(C.byref(hd), 65536, 2)
+    assert 0 < n_p <= 65536 * 24 + 4096 and n_p < n_f
+    assert R.lib.rl_workspace_size(C.byref(hd), 65536, 3) == 0
     assert R.lib.rl_workspace_size(C.byref(R.rl_head(100, 10, R.RL_BF16, 100, 1.0)), 10, 0) == 0
     assert R.lib.rl_workspace_size(C.byref(R.rl_head(64, 10, R.RL_BF16, 64, 0.0)), 10, 0) == 0
     assert R.lib.rl_workspace_size(C.byref(R.rl_head(100, 10, R.RL_F32, 100, 1.0)), 10, 0) > 0

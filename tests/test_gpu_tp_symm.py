@@ -53,7 +53,9 @@ def test_dp2_fused_dw_reduce_scatter(empty_last):
     import torch
     if torch.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs")
-    res = _dp_check(["--config", "qwen1.5b", "--max-mb", "2", "--mb-rows", "8192", "--reps", "1"]
+    # 2 x 32k rows: several whole groups per rank (the first two groups of the
+    # generator are forced all-correct / all-wrong, A = 0)
+    res = _dp_check(["--config", "qwen1.5b", "--max-mb", "2", "--mb-rows", "32768", "--reps", "1"]
                     + (["--empty-last"] if empty_last else []))
     m = res["modes"]
     assert res["norm_dW"] > 0 and m["symm"]["rel_dW_vs_nccl"] <= 1e-6, res
@@ -64,7 +66,11 @@ def test_dp2_fused_dw_reduce_scatter(empty_last):
 def test_dp2_split_groups():
     """Split-group sharding (sequences, not whole groups, are
     LPT-assigned; group statistics all-reduced by global id): the whole-batch
-    dW and token count equal the group-sharded step's (same global rows)."""
+    dW and token count equal the group-sharded step's (same global rows).
+    Different micro-batch composition reorders the fp32 accumulation of a dW
+    with heavy sign cancellation (measured rel 2.6e-5 at qwen1.5b); a wrong or
+    local-only group statistic or a lost partial is O(1), so 1e-3 (10x below
+    the 1e-2 gradient tolerance) still discriminates."""
     import torch
     if torch.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs")
@@ -73,7 +79,29 @@ def test_dp2_split_groups():
     m = res["modes"]
     assert res["norm_dW"] > 0
     for k in ("nccl-split", "symm-split"):
-        assert m[k]["rel_dW_vs_nccl"] <= 1e-5, res
+        assert m[k]["rel_dW_vs_nccl"] <= 1e-3, res
         assert m[k]["tokens"] == m["nccl"]["tokens"], res
         assert abs(m[k]["loss_sum"] - m["nccl"]["loss_sum"]) <= 1e-6 * abs(m["nccl"]["loss_sum"]) + 1e-6
+    assert all(v["ranks_identical_dW"] for v in m.values()), res
+
+
+def test_dp2_streaming_fused_reduce_scatter():
+    """NEXT-2 streaming interface with the fused dW reduce-scatter: last=True on
+    the final feed, or (-nolast) finish() shipping the partial through a masked
+    one-row micro-batch; dW (deferred 1/N) matches the step's within the bf16
+    gradient tolerance (1e-2): the unscaled g rounds dZ to bf16 differently
+    from the 1/N-scaled one (2^-9 per element; measured rel 1.8e-3 at
+    qwen1.5b). The three streaming variants must agree with each other
+    bit for bit (same dZ, same rank-order / NCCL sums at P = 2)."""
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    res = _dp_check(["--config", "qwen1.5b", "--max-mb", "3", "--mb-rows", "16384", "--reps", "1",
+                     "--modes", "nccl,stream-nccl,stream-symm,stream-symm-nolast"])
+    m = res["modes"]
+    assert res["norm_dW"] > 0
+    for k in ("stream-nccl", "stream-symm", "stream-symm-nolast"):
+        assert m[k]["rel_dW_vs_nccl"] <= 1e-2, res
+        assert m[k]["rel_dW_vs_nccl"] == m["stream-nccl"]["rel_dW_vs_nccl"], res
+        assert m[k]["tokens"] == m["nccl"]["tokens"], res
     assert all(v["ranks_identical_dW"] for v in m.values()), res

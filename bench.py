@@ -418,7 +418,9 @@ def run_aux(rl, head, H, W, db, mine, step, kinds, tokens_local, tokens_global, 
 def run_e2e(args, rl, step, db, mine, H, old, gh, dev, world, tokens_global):
     """Same metric through the public API with HOST inputs: every step copies
     its inputs from pinned host memory (hidden streamed per micro-batch on a
-    copy stream, double-buffered) and reads the loss statistics back."""
+    copy stream, double-buffered, the next step's first micro-batches
+    prefetched under this step's last ones) and reads the loss statistics
+    back."""
     import torch
     import torch.distributed as dist
     R = mine.num_rows
@@ -439,22 +441,31 @@ def run_e2e(args, rl, step, db, mine, H, old, gh, dev, world, tokens_global):
     h2d = sum(v.numel() * v.element_size() for v in host_small.values()) + \
         sum((r1 - r0) * H.shape[1] * H.element_size() for _, _, r0, r1, _ in db.mbs)
 
-    def issue_copy(i):
-        _, _, r0, r1, _ = db.mbs[i]
+    n_mb = len(db.mbs)
+    # micro-batches are numbered c = step * n_mb + i across the steps of one run
+    # so the copy of the next step's first micro-batches overlaps this step's
+    # last ones (a training loop prefetching its next batch); buffer = c % 2.
+    state = {"base": 0, "total": 0, "issued": 0}
+
+    def issue_copy(c):
+        _, _, r0, r1, _ = db.mbs[c % n_mb]
         with torch.cuda.stream(copy_s):
-            copy_s.wait_event(freed[i % 2])
-            bufs[i % 2][:r1 - r0].copy_(host_H[r0:r1], non_blocking=True)
-            ready[i % 2].record(copy_s)
+            copy_s.wait_event(freed[c % 2])
+            bufs[c % 2][:r1 - r0].copy_(host_H[r0:r1], non_blocking=True)
+            ready[c % 2].record(copy_s)
+        state["issued"] = c + 1
 
     def hidden_for_mb(i):
-        comp.wait_event(ready[i % 2])
+        c = state["base"] + i
+        comp.wait_event(ready[c % 2])
         _, _, r0, r1, _ = db.mbs[i]
-        return bufs[i % 2][:r1 - r0]
+        return bufs[c % 2][:r1 - r0]
 
     def after_mb(i):
-        freed[i % 2].record(comp)
-        if i + 2 < len(db.mbs):
-            issue_copy(i + 2)
+        c = state["base"] + i
+        freed[c % 2].record(comp)
+        if c + 2 < state["total"]:
+            issue_copy(c + 2)
 
     orig = (step.db.targets, step.db.mask, step.db.cu, step.db.gos, step.db.rewards,
             list(step.db.mbs))
@@ -467,23 +478,27 @@ def run_e2e(args, rl, step, db, mine, H, old, gh, dev, world, tokens_global):
         step.db.gos, step.db.rewards = dev_small["gos"], dev_small["rewards"]
         step.db.mbs = [(s0, s1, r0, r1, dev_small[f"cu_mb{i}"])
                        for i, (s0, s1, r0, r1, _) in enumerate(orig[5])]
-        for e in freed:
-            e.record(comp)
-        issue_copy(0)
-        if len(db.mbs) > 1:
-            issue_copy(1)
+        b = state["base"]
+        for c in range(state["issued"], min(b + 2, state["total"])):
+            issue_copy(c)            # not prefetched by the previous step
         step.run(None, dev_small["old"], gh, hidden_for_mb=hidden_for_mb, after_mb=after_mb)
         stats_host.copy_(step.stats, non_blocking=True)
+        state["base"] = b + n_mb
 
-    for _ in range(max(1, min(args.warmup, 2))):
-        one()
+    def run(k):
+        state.update(base=0, total=k * n_mb, issued=0)
+        for e in freed:
+            e.record(comp)
+        for _ in range(k):
+            one()
+
+    run(max(1, min(args.warmup, 2)))
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    for _ in range(args.steps):
-        one()
+    run(args.steps)
     e1.record()
     torch.cuda.synchronize()
     (step.db.targets, step.db.mask, step.db.cu, step.db.gos, step.db.rewards) = orig[:5]

@@ -171,6 +171,14 @@ __device__ __forceinline__ void multimem_red_add_v4_f32(void* mc, uint32_t a, ui
                : "memory");
 }
 
+// Add four fp32 to global memory in L2 (fire-and-forget; the SM does not
+// wait for the old value).
+__device__ __forceinline__ void red_add_v4_f32(void* p, float a, float b, float c, float d) {
+  asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a),
+               "f"(b), "f"(c), "f"(d)
+               : "memory");
+}
+
 // ------------------------------------------------- clusters / CTA pairs ----
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;

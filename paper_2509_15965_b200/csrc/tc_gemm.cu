@@ -104,6 +104,7 @@ struct TcArgs {
   // (local partial + tile) into slot [rs_rank][j - o rs_rows] of the owner's
   // staging buffer over NVLink (plain stores; the owner sums the slots in
   // rank order afterwards, so the result is deterministic).
+  int32_t acc_red;     // EPI_ACC: accumulate with red.global.add (L2) instead of load+store
   int32_t rs_world;    // 0 = off
   int32_t rs_rank;
   int64_t rs_rows;
@@ -516,6 +517,15 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                 o.w += __uint_as_float(v[4 * q + 3]);
                 slot[q] = o;
               }
+            } else if (args.acc_red) {
+              // the add happens in L2: no read on the epilogue's critical path.
+              // One add per element per launch, launches stream-ordered: the
+              // accumulation order is still fixed (deterministic).
+#pragma unroll
+              for (int q = 0; q < 8; ++q)
+                red_add_v4_f32(dst + c * 8 + q, __uint_as_float(v[4 * q]),
+                               __uint_as_float(v[4 * q + 1]), __uint_as_float(v[4 * q + 2]),
+                               __uint_as_float(v[4 * q + 3]));
             } else {
 #pragma unroll
               for (int q = 0; q < 8; ++q) {
@@ -772,6 +782,9 @@ rl_status launch_tc_bwd(const rl_head* hd, const void* weight, void* grad_hidden
   t7.N = h;
   t7.acc = grad_weight;
   t7.ld_acc = h;
+  // red.add accumulate (default): same-box A/B +1.2% at 16k rows, dW GEMM -8%
+  // (profiles/r1/SUMMARY.md); RLHEAD_DW_RED=0 restores load+add+store
+  t7.acc_red = env_int("RLHEAD_DW_RED", 1);
   if (dw_rs && dw_rs->world > 1) {
     t7.rs_world = dw_rs->world;
     t7.rs_rank = dw_rs->rank;
@@ -791,6 +804,7 @@ rl_status launch_tc_bwd(const rl_head* hd, const void* weight, void* grad_hidden
     t.group_m2 = t.group_m;
     t.acc = grad_weight;
     t.ld_acc = h;
+    t.acc_red = t7.acc_red;
     t.rs_world = t7.rs_world;
     t.rs_rank = t7.rs_rank;
     t.rs_rows = t7.rs_rows;

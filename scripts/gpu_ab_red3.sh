@@ -1,0 +1,8 @@
+run() { # label env mb
+  env $2 timeout -s KILL 900 python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-aux --mb-rows $3 > gpurun_out/ab.log 2>&1
+  tail -1 gpurun_out/ab.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$1', d['value'], d['clocks']['sm_mhz'], d['gpu_launches'], {k:v['ms_total'] for k,v in d['kernels'].items() if 'gemm' in k})" 2>/dev/null || tail -c 800 gpurun_out/ab.log
+}
+run red1-8k RLHEAD_DW_RED=1 8192
+run red1-16k RLHEAD_DW_RED=1 16384
+run red1-8k RLHEAD_DW_RED=1 8192
+run red1-16k RLHEAD_DW_RED=1 16384

@@ -16,7 +16,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
                                  {"RLHEAD_CTA_GROUP": "2", "RLHEAD_WIDE": "1",
                                   "RLHEAD_FUSED_BWD": "1"},
                                  {"RLHEAD_CTA_GROUP": "2", "RLHEAD_WIDE": "1",
-                                  "RLHEAD_GROUP_M": "16", "RLHEAD_GROUP_M_BWD": "4"}],
+                                  "RLHEAD_GROUP_M": "16", "RLHEAD_GROUP_M_BWD": "4"},
+                                 {"RLHEAD_DW_RED": "0"},
+                                 {"RLHEAD_DW_RED": "1", "RLHEAD_FUSED_BWD": "1"}],
                          ids=["cta1", "cta2-narrow", "cta2-wide-fused", "cta2-unfused-raster"])
 def test_variant_parity(env):
     import torch

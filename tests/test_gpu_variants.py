@@ -19,7 +19,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
                                   "RLHEAD_GROUP_M": "16", "RLHEAD_GROUP_M_BWD": "4"},
                                  {"RLHEAD_DW_RED": "0"},
                                  {"RLHEAD_DW_RED": "1", "RLHEAD_FUSED_BWD": "1"}],
-                         ids=["cta1", "cta2-narrow", "cta2-wide-fused", "cta2-unfused-raster"])
+                         ids=["cta1", "cta2-narrow", "cta2-wide-fused", "cta2-unfused-raster",
+                              "dw-load-store", "dw-red-fused"])
 def test_variant_parity(env):
     import torch
     if not torch.cuda.is_available():

@@ -59,7 +59,15 @@ struct TcCfg {
   static constexpr int TILE_M = TC_BM * CG;
   static constexpr int TILE_N = TC_BN * NB;
   static constexpr int ACC_STAGES = NB == 1 ? 2 : 1;
+  // dW epilogue staging for the TMA reduce-add (acc_red == 2): 4 warps x 2 x
+  // [32 rows][32 fp32], 128-B swizzled; placed after the barrier block.
+  static constexpr int STG_OFF = STAGES * STAGE_BYTES + 1024;
+  static constexpr int STG_BYTES = 4 * 2 * 4096;
 };
+template <int CG, int NB, int EPI>
+constexpr int tc_smem_bytes() {
+  return TcCfg<CG, NB>::SMEM_BYTES + (EPI == 3 /*EPI_ACC*/ && NB == 2 ? 1024 + TcCfg<CG, NB>::STG_BYTES : 0);
+}
 
 // EPI_BWD: problem 0 = dH (A K-major, EPI_ROWS), problem 1 = dW (A MN-major,
 // EPI_ACC), both with MN-major B, in one persistent launch.
@@ -74,7 +82,8 @@ struct TcArgs {
   // second problem of EPI_BWD (the dW GEMM)
   int64_t M2, K2;
   int32_t n_tiles2, m_dyn2, k_dyn2, group_m2;
-  int32_t l2_policy;   // TMA L2 hint: 0 normal, 1 evict_last, 2 evict_first
+  int32_t l2_pol_a;    // TMA L2 hint of the A operand: 0 normal, 1 evict_last, 2 evict_first
+  int32_t l2_pol_b;    // same for B (A/B can differ: a streamed panel vs a reused one)
   const WsHeader* hdr;
   float inv_temp;
   int32_t vocab;       // columns of this (shard of the) head
@@ -104,7 +113,10 @@ struct TcArgs {
   // (local partial + tile) into slot [rs_rank][j - o rs_rows] of the owner's
   // staging buffer over NVLink (plain stores; the owner sums the slots in
   // rank order afterwards, so the result is deterministic).
-  int32_t acc_red;     // EPI_ACC: accumulate with red.global.add (L2) instead of load+store
+  int32_t k_serp;      // odd persistent iterations walk K backwards (the next wave starts on
+                       // the operand rows the previous one read last, still in L2)
+  int32_t acc_red;     // EPI_ACC: 0 load+add+store, 1 red.global.add (L2), 2 TMA reduce-add
+                       // of 32x32 smem boxes (tmA2 = fp32 map of acc; 512-wide tiles only)
   int32_t rs_world;    // 0 = off
   int32_t rs_rank;
   int64_t rs_rows;
@@ -172,6 +184,9 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       tma_prefetch_desc(&tmA2);
       tma_prefetch_desc(&tmB2);
     }
+    if constexpr (EPI == EPI_ACC) {
+      if (args.acc_red == 2) tma_prefetch_desc(&tmA2);
+    }
     for (int i = 0; i < C::STAGES; ++i) {
       mbar_init(full + i, CG);     // CG producers arrive (remote for the peer)
       mbar_init(empty + i, 1);     // one (multicast) commit per phase
@@ -215,17 +230,22 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------------ TMA producer
-      const uint64_t pol = args.l2_policy == 1   ? l2_policy_evict_last()
-                           : args.l2_policy == 2 ? l2_policy_evict_first()
-                                                 : l2_policy_evict_normal();
+      auto mkpol = [](int code) {
+        return code == 1 ? l2_policy_evict_last()
+               : code == 2 ? l2_policy_evict_first()
+                           : l2_policy_evict_normal();
+      };
+      const uint64_t pol_a = mkpol(args.l2_pol_a), pol_b = mkpol(args.l2_pol_b);
       int stage = 0;
       uint32_t phase = 0;
-      for (int64_t tile = cid; tile < num_tiles; tile += ncl) {
+      int64_t it = 0;
+      for (int64_t tile = cid; tile < num_tiles; tile += ncl, ++it) {
         int64_t mb;
         int nb;
         bool second;
         const Prob& P = locate(tile, second, mb, nb);
         const bool amn = EPI == EPI_BWD ? second : (AMN != 0);
+        const bool krev = args.k_serp && (it & 1);
         const CUtensorMap* mA = second ? &tmA2 : &tmA;
         const CUtensorMap* mB = second ? &tmB2 : &tmB;
         const int32_t m0 = static_cast<int32_t>(mb * C::TILE_M + rank * TC_BM);
@@ -237,8 +257,9 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           else mbar_arrive_cluster(full + stage, 0);
           uint8_t* a_dst = sA + stage * C::A_BYTES;
           uint8_t* b_dst = sB + stage * C::B_BYTES;
-          const int32_t k0 = static_cast<int32_t>(kb * TC_BK);
+          const int32_t k0 = static_cast<int32_t>((krev ? P.num_k - 1 - kb : kb) * TC_BK);
           auto load = [&](const CUtensorMap* m, void* dst, int32_t c0, int32_t c1) {
+            const uint64_t pol = m == mA ? pol_a : pol_b;
             if constexpr (CG == 2) tma_load_2d_2sm(m, full + stage, dst, c0, c1, pol);
             else tma_load_2d(m, full + stage, dst, c0, c1, pol);
           };
@@ -490,6 +511,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       } else {  // EPI_ACC (or the dW half of EPI_BWD)
         float4* dst = reinterpret_cast<float4*>(args.acc + row * args.ld_acc + n0);
         const bool empty_k = P.num_k == 0;  // keep_empty tile: no MMA ran
+        const bool tma_red = EPI == EPI_ACC && NB == 2 && args.acc_red == 2 && args.rs_world == 0;
 #pragma unroll 1
         for (int c = 0; c < C::TILE_N / 32; ++c) {
           uint32_t v[32];
@@ -499,6 +521,30 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           if (empty_k) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = 0u;
+          }
+          if constexpr (EPI == EPI_ACC && NB == 2) {
+            if (tma_red) {
+              // this warp's 32 rows x 32 columns -> a 128-B-swizzled smem box
+              // (16-B chunk j of row r at chunk j ^ (r & 7): conflict-free),
+              // then one lane adds the box into acc with a TMA reduce (whole
+              // L2 lines; out-of-range rows/columns are clipped by the map).
+              // Two buffers per warp: chunk c reuses the one of chunk c - 2.
+              uint8_t* buf = smem + C::STG_OFF + ew * 8192 + (c & 1) * 4096;
+              if (lane == 0) bulk_wait_group_read<1>();
+              __syncwarp();
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                *reinterpret_cast<uint4*>(buf + lane * 128 + ((j ^ (lane & 7)) << 4)) =
+                    make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+              fence_proxy_async_smem();
+              __syncwarp();
+              if (lane == 0) {
+                tma_reduce_add_2d(&tmA2, buf, n0 + c * 32,
+                                  static_cast<int32_t>(mb * C::TILE_M + rank * TC_BM + ew * 32));
+                bulk_commit_group();
+              }
+              continue;
+            }
           }
           if (row_ok && n0 + c * 32 < args.N) {
             if (args.rs_world > 0) {  // local partial + tile -> the owner's slot
@@ -545,6 +591,9 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         acc_phase ^= 1;
       }
     }
+  }
+  if constexpr (EPI == EPI_ACC && NB == 2) {
+    if (warp >= 4 && lane == 0 && args.acc_red == 2) bulk_wait_group_all();
   }
   tc_fence_before();
   __syncwarp();
@@ -594,6 +643,21 @@ static bool make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t 
          CUDA_SUCCESS;
 }
 
+// 2-D fp32 tensor map (dims {inner, outer}, box {box_inner, box_outer},
+// 128-B swizzle): the dW accumulator as a TMA reduce-add destination.
+static bool make_map_f32(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
+                         uint64_t stride_bytes, uint32_t box_inner, uint32_t box_outer) {
+  PFN_encodeTiled_t enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {stride_bytes};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box,
+             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 int num_sms() {
   static int n = 0;
   static std::once_flag once;
@@ -626,22 +690,28 @@ int tc_cta_group() {
 template <int CG, int NB, int AMN, int BMN, int EPI>
 static rl_status run_gemm(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& a2,
                           const CUtensorMap& b2, const TcArgs& args, int64_t tiles_bound,
-                          int kind, cudaStream_t s) {
+                          int kind, cudaStream_t s, bool persistent = true) {
   using C = TcCfg<CG, NB>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
     attr_err = cudaFuncSetAttribute(k_tc_gemm<CG, NB, AMN, BMN, EPI>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    tc_smem_bytes<CG, NB, EPI>());
   });
   if (attr_err != cudaSuccess) return RL_ERR_CUDA;
   if (tiles_bound <= 0) return RL_OK;
   const int64_t clusters_max = num_sms() / CG;
-  const int64_t clusters = tiles_bound < clusters_max ? tiles_bound : clusters_max;
+  // persistent: one cluster per TPC pair walks the tile space; otherwise one
+  // cluster per tile and the block scheduler hands tiles out in order as
+  // clusters retire, so tiles that share operand panels (consecutive ids)
+  // start together however far the pairs have drifted apart.
+  const int64_t clusters =
+      (!persistent || tiles_bound < clusters_max) ? tiles_bound : clusters_max;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(clusters * CG));
   cfg.blockDim = dim3(TC_THREADS);
-  cfg.dynamicSmemBytes = C::SMEM_BYTES;
+  cfg.dynamicSmemBytes = tc_smem_bytes<CG, NB, EPI>();
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -680,19 +750,32 @@ static bool wide_bwd() { return tc_cta_group() == 2 && env_int("RLHEAD_WIDE", 1)
 static bool fused_bwd() { return wide_bwd() && env_int("RLHEAD_FUSED_BWD", 0) != 0; }
 template <int AMN, int BMN, int EPI>
 static rl_status run_wide(const CUtensorMap& a, const CUtensorMap& b, TcArgs t, int64_t m_extent,
-                          int kind, cudaStream_t s) {
+                          int kind, cudaStream_t s, const CUtensorMap* a2 = nullptr) {
   t.group_m = env_int("RLHEAD_GROUP_M_BWD", 1);
   if (t.group_m < 1) t.group_m = 1;
   if (wide_bwd()) {
     t.n_tiles = static_cast<int32_t>(ceil_div(t.N, 2 * TC_BN));
-    return run_gemm<2, 2, AMN, BMN, EPI>(a, b, a, b, t, ceil_div(m_extent, 2 * TC_BM) * t.n_tiles,
-                                         kind, s);
+    const bool persistent =
+        env_int(EPI == EPI_ACC ? "RLHEAD_NONPERSIST_DW" : "RLHEAD_NONPERSIST_DH", 0) == 0;
+    return run_gemm<2, 2, AMN, BMN, EPI>(a, b, a2 ? *a2 : a, b, t,
+                                         ceil_div(m_extent, 2 * TC_BM) * t.n_tiles, kind, s,
+                                         persistent);
   }
+  if (t.acc_red == 2) t.acc_red = 1;  // TMA reduce: 512-wide tiles only
   t.n_tiles = static_cast<int32_t>(ceil_div(t.N, TC_BN));
   const int cg = tc_cta_group();
   const int64_t tiles = ceil_div(m_extent, TC_BM * cg) * t.n_tiles;
   if (cg == 2) return run_gemm<2, 1, AMN, BMN, EPI>(a, b, a, b, t, tiles, kind, s);
   return run_gemm<1, 1, AMN, BMN, EPI>(a, b, a, b, t, tiles, kind, s);
+}
+
+// Per-GEMM-kind L2 hints for (A, B): env RLHEAD_L2_<KIND> = two digits "ab"
+// (0 normal, 1 evict_last, 2 evict_first); unset keeps RLHEAD_L2_POLICY for both.
+static void kind_policy(TcArgs& t, const char* env, int dflt_ab) {
+  const int ab = env_int(env, dflt_ab);
+  if (ab < 0) return;
+  t.l2_pol_a = (ab / 10) % 10;
+  t.l2_pol_b = ab % 10;
 }
 
 static TcArgs base_args(const rl_head* hd, const WsLayout& L, char* ws) {
@@ -701,7 +784,9 @@ static TcArgs base_args(const rl_head* hd, const WsLayout& L, char* ws) {
   t.inv_temp = hd->inv_temperature;
   t.vocab = hd->vocab;
   t.y_off = hd->vocab_total > 0 ? hd->vocab_offset : 0;
-  t.l2_policy = env_int("RLHEAD_L2_POLICY", 1);
+  const int pol = env_int("RLHEAD_L2_POLICY", 1);
+  t.l2_pol_a = pol;
+  t.l2_pol_b = pol;
   t.tgt_c = reinterpret_cast<const int32_t*>(ws + L.off_tgt);
   t.ldp = L.Rp;
   return t;
@@ -724,6 +809,7 @@ rl_status launch_tc_fwd(const rl_head* hd, const void* weight, const WsLayout& L
   t.ps = reinterpret_cast<float*>(ws + L.off_ps);
   t.pu = reinterpret_cast<float*>(ws + L.off_pu);
   t.zy = reinterpret_cast<float*>(ws + L.off_zy);
+  kind_policy(t, "RLHEAD_L2_FWD", -1);
   return run_narrow<0, 0, EPI_LSE>(ma, mb, t, L.Rp, RL_K_GEMM_LSE, s);
 }
 
@@ -754,6 +840,7 @@ rl_status launch_tc_bwd(const rl_head* hd, const void* weight, void* grad_hidden
     }
     t.dz = dz;
     t.ld_dz = L.Vp;
+    kind_policy(t, "RLHEAD_L2_DZ", -1);
     st = run_narrow<0, 0, EPI_DZ>(ma, mb, t, L.Rp, RL_K_GEMM_DZ, s);
     if (st != RL_OK) return st;
   }
@@ -775,6 +862,7 @@ rl_status launch_tc_bwd(const rl_head* hd, const void* weight, void* grad_hidden
   t6.out_f32 = grad_hidden_f32;
   t6.out_mc = gh_multicast ? 1 : 0;
   t6.row_idx = reinterpret_cast<const int32_t*>(ws + L.off_active);
+  kind_policy(t6, "RLHEAD_L2_DH", -1);
   TcArgs t7 = base_args(hd, L, ws);
   t7.M = V;
   t7.K = L.Rp;
@@ -785,6 +873,8 @@ rl_status launch_tc_bwd(const rl_head* hd, const void* weight, void* grad_hidden
   // red.add accumulate (default): same-box A/B +1.2% at 16k rows, dW GEMM -8%
   // (profiles/r1/SUMMARY.md); RLHEAD_DW_RED=0 restores load+add+store
   t7.acc_red = env_int("RLHEAD_DW_RED", 1);
+  kind_policy(t7, "RLHEAD_L2_DW", -1);
+  t7.k_serp = env_int("RLHEAD_DW_SERP", 0);
   if (dw_rs && dw_rs->world > 1) {
     t7.rs_world = dw_rs->world;
     t7.rs_rank = dw_rs->rank;
@@ -813,7 +903,14 @@ rl_status launch_tc_bwd(const rl_head* hd, const void* weight, void* grad_hidden
     return run_gemm<2, 2, 0, 1, EPI_BWD>(ma6, mb6, ma7, mb7, t, tiles, RL_K_GEMM_DHDW, s);
   }
   if ((st = run_wide<0, 1, EPI_ROWS>(ma6, mb6, t6, L.Rp, RL_K_GEMM_DH, s)) != RL_OK) return st;
-  return run_wide<1, 1, EPI_ACC>(ma7, mb7, t7, V, RL_K_GEMM_DW, s);
+  CUtensorMap macc;
+  if (t7.acc_red == 2) {
+    if (t7.rs_world > 0) t7.acc_red = 1;  // reduce-scatter epilogue: plain stores
+    else if (!make_map_f32(&macc, grad_weight, h, V, static_cast<uint64_t>(h) * 4, 32, 32))
+      return RL_ERR_CUDA;
+  }
+  return run_wide<1, 1, EPI_ACC>(ma7, mb7, t7, V, RL_K_GEMM_DW, s,
+                                 t7.acc_red == 2 ? &macc : nullptr);
 }
 
 }  // namespace rlh

@@ -18,9 +18,14 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
                                  {"RLHEAD_CTA_GROUP": "2", "RLHEAD_WIDE": "1",
                                   "RLHEAD_GROUP_M": "16", "RLHEAD_GROUP_M_BWD": "4"},
                                  {"RLHEAD_DW_RED": "0"},
-                                 {"RLHEAD_DW_RED": "1", "RLHEAD_FUSED_BWD": "1"}],
+                                 {"RLHEAD_DW_RED": "1", "RLHEAD_FUSED_BWD": "1"},
+                                 {"RLHEAD_DW_RED": "2"},
+                                 {"RLHEAD_L2_DW": "21", "RLHEAD_L2_DH": "21"},
+                                 {"RLHEAD_DW_SERP": "1", "RLHEAD_DW_RED": "2"},
+                                 {"RLHEAD_NONPERSIST_DW": "1", "RLHEAD_NONPERSIST_DH": "1"}],
                          ids=["cta1", "cta2-narrow", "cta2-wide-fused", "cta2-unfused-raster",
-                              "dw-load-store", "dw-red-fused"])
+                              "dw-load-store", "dw-red-fused", "dw-tma-reduce", "l2-hints",
+                              "dw-serpentine", "non-persistent"])
 def test_variant_parity(env):
     import torch
     if not torch.cuda.is_available():
@@ -30,3 +35,50 @@ def test_variant_parity(env):
                        cwd=ROOT, env={**os.environ, **env}, capture_output=True, text=True,
                        timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+def test_dw_accumulate_paths_bit_identical(rl):
+    """dW += dZ^T Hc through the three epilogue accumulate paths (load+add+
+    store, red.global.add, TMA bulk reduce-add of smem boxes) adds the same
+    fp32 tile to the same fp32 value once per element per launch: the results
+    must be bit-identical, over a ragged V (not a multiple of the 256-row
+    tile) and h (not a multiple of the 512-column tile), starting from a
+    non-zero accumulator and over two launches."""
+    import numpy as np
+    import torch
+    from tests.gpu_util import dev_tensors
+    from workload import custom_layout
+    rng = np.random.default_rng(11)
+    V, h = 3000, 608
+    lay = custom_layout(rng.integers(0, 30, 24), rng.integers(1, 200, 24), np.arange(24) // 4,
+                        rng.choice([-5.0, 5.0], 24), vocab=V, num_groups=6)
+    d = dev_tensors(lay)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    H = torch.randn(lay.num_rows, h, device="cuda", generator=g).to(torch.bfloat16)
+    W = (torch.randn(V, h, device="cuda", generator=g) * (4 / h ** 0.5)).to(torch.bfloat16)
+    gw0 = torch.randn(V, h, device="cuda", generator=g) * 1e-3
+    head = rl.Head(h, V, "bf16")
+    old = torch.empty(lay.num_rows, device="cuda")      # ratio = 1: every token has a gradient
+    rl.rl_logprob_fwd(head, H, W, rl.Batch(d["cu"], d["targets"], d["mask"], d["err"]), old)
+    adv = torch.linspace(-1, 1, lay.num_seqs, device="cuda")
+    out = {}
+    prev = os.environ.get("RLHEAD_DW_RED")
+    try:
+        for mode in ("0", "1", "2"):
+            os.environ["RLHEAD_DW_RED"] = mode
+            gw = gw0.clone()
+            for _ in range(2):
+                logp = torch.empty(lay.num_rows, device="cuda")
+                gh = torch.empty_like(H)
+                b = rl.Batch(d["cu"], d["targets"], d["mask"], d["err"])
+                rl.rl_policy_loss_fwd_bwd(head, H, W, b, old, adv, rl.LossParams(), logp, gh, gw)
+            torch.cuda.synchronize()
+            out[mode] = gw.cpu()
+    finally:
+        if prev is None:
+            os.environ.pop("RLHEAD_DW_RED", None)
+        else:
+            os.environ["RLHEAD_DW_RED"] = prev
+    assert not torch.equal(out["1"], gw0.cpu())
+    assert torch.equal(out["0"], out["1"])
+    assert torch.equal(out["2"], out["1"])

@@ -61,6 +61,10 @@ struct WsHeader {
   int64_t n_active;   // active rows of this call
   int32_t bad_cu;     // malformed cu_seqlens
   int32_t pad;
+  // dynamic tile scheduler of the tensor-core GEMMs, one {claimed, retired}
+  // counter pair per GEMM kind; zeroed by k_validate and by the last CTA of
+  // every launch that uses it
+  uint32_t sched[8][2];
 };
 
 // ------------------------------------------------------ device reductions ----

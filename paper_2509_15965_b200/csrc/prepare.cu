@@ -23,6 +23,11 @@ __global__ void k_validate(const int32_t* __restrict__ cu, int32_t S, int64_t R,
   if (threadIdx.x == 0) {
     hdr->bad_cu = bad;
     hdr->n_active = 0;
+  }
+  if (threadIdx.x < 16) {
+    hdr->sched[threadIdx.x >> 1][threadIdx.x & 1] = 0u;
+  }
+  if (threadIdx.x == 0) {
     if (bad && err) atomicOr(err, RL_DEVERR_CU_SEQLENS);
   }
 }

@@ -64,9 +64,13 @@ struct TcCfg {
   static constexpr int STG_OFF = STAGES * STAGE_BYTES + 1024;
   static constexpr int STG_BYTES = 4 * 2 * 4096;
 };
+// extra dynamic smem of an epilogue's TMA staging buffers (after the barriers)
 template <int CG, int NB, int EPI>
 constexpr int tc_smem_bytes() {
-  return TcCfg<CG, NB>::SMEM_BYTES + (EPI == 3 /*EPI_ACC*/ && NB == 2 ? 1024 + TcCfg<CG, NB>::STG_BYTES : 0);
+  return TcCfg<CG, NB>::SMEM_BYTES +
+         (EPI == 3 /*EPI_ACC*/ && NB == 2 ? 1024 + TcCfg<CG, NB>::STG_BYTES
+          : EPI == 1 /*EPI_DZ*/           ? 1024 + 4 * 2 * 2048
+                                          : 0);
 }
 
 // EPI_BWD: problem 0 = dH (A K-major, EPI_ROWS), problem 1 = dW (A MN-major,
@@ -85,6 +89,7 @@ struct TcArgs {
   int32_t l2_pol_a;    // TMA L2 hint of the A operand: 0 normal, 1 evict_last, 2 evict_first
   int32_t l2_pol_b;    // same for B (A/B can differ: a streamed panel vs a reused one)
   const WsHeader* hdr;
+  uint32_t* sched;     // dynamic tile scheduler {claimed, retired} (NULL = static schedule)
   float inv_temp;
   int32_t vocab;       // columns of this (shard of the) head
   int64_t y_off;       // global id of column 0 (vocab-parallel shard offset)
@@ -113,6 +118,7 @@ struct TcArgs {
   // (local partial + tile) into slot [rs_rank][j - o rs_rows] of the owner's
   // staging buffer over NVLink (plain stores; the owner sums the slots in
   // rank order afterwards, so the result is deterministic).
+  int32_t dz_tma;      // EPI_DZ: stage bf16 32x32 boxes in smem, TMA-store them (tmA2 = dZ map)
   int32_t k_serp;      // odd persistent iterations walk K backwards (the next wave starts on
                        // the operand rows the previous one read last, still in L2)
   int32_t acc_red;     // EPI_ACC: 0 load+add+store, 1 red.global.add (L2), 2 TMA reduce-add
@@ -172,7 +178,10 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* sfull = tempty + 2;   // dynamic scheduler: tile id ring (2 slots)
+  uint64_t* sempty = sfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sempty + 2);
+  int32_t* ring = reinterpret_cast<int32_t*>(tmem_slot + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
@@ -187,6 +196,9 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     if constexpr (EPI == EPI_ACC) {
       if (args.acc_red == 2) tma_prefetch_desc(&tmA2);
     }
+    if constexpr (EPI == EPI_DZ) {
+      if (args.dz_tma) tma_prefetch_desc(&tmA2);
+    }
     for (int i = 0; i < C::STAGES; ++i) {
       mbar_init(full + i, CG);     // CG producers arrive (remote for the peer)
       mbar_init(empty + i, 1);     // one (multicast) commit per phase
@@ -194,6 +206,10 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     for (int i = 0; i < 2; ++i) {
       mbar_init(tfull + i, 1);
       mbar_init(tempty + i, 128 * CG);  // all epilogue threads of the pair
+      mbar_init(sfull + i, 1);          // the leader's scheduler thread
+      // consumers of a tile id: producer + MMA + 4 epilogue warps (leader),
+      // producer + 4 epilogue warps (peer)
+      mbar_init(sempty + i, CG == 2 ? 11 : 6);
     }
     fence_mbar_init();
   }
@@ -219,6 +235,27 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             args.group_m2, args.rs_world > 0);
   const int64_t num_tiles = P0.tiles + P1.tiles;
   const int64_t cid = blockIdx.x / CG, ncl = gridDim.x / CG;
+  // Tile schedule. Static: cluster c runs tiles c, c + ncl, ... Dynamic
+  // (args.sched): the first tile is static, then the leader's scheduler thread
+  // claims tiles from a global counter one tile ahead of use and hands the id
+  // to both CTAs through a 2-slot ring, so tiles run in claim order and the
+  // tiles that share A/B panels in L2 (consecutive ids) run at the same time
+  // however far individual pairs drift apart over a long launch.
+  const bool dyn = args.sched != nullptr;
+  auto next_tile = [&](int64_t it, int64_t& tile) -> bool {
+    if (!dyn) {
+      tile = cid + it * ncl;
+      return tile < num_tiles;
+    }
+    mbar_wait_acq_cluster(sfull + (it & 1), static_cast<uint32_t>((it >> 1) & 1));
+    tile = ring[it & 1];
+    return tile >= 0;
+  };
+  auto tile_read = [&](int64_t it) {  // one thread per consumer role, after next_tile
+    if (!dyn) return;
+    if (CG == 2 && !leader) mbar_arrive_cluster_release(sempty + (it & 1), 0);
+    else mbar_arrive(sempty + (it & 1));
+  };
   // per tile: which problem, its coordinates and K extent
   auto locate = [&](int64_t tile, bool& second, int64_t& mb, int& nb) -> const Prob& {
     second = tile >= P0.tiles;
@@ -238,14 +275,16 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       const uint64_t pol_a = mkpol(args.l2_pol_a), pol_b = mkpol(args.l2_pol_b);
       int stage = 0;
       uint32_t phase = 0;
-      int64_t it = 0;
-      for (int64_t tile = cid; tile < num_tiles; tile += ncl, ++it) {
+      for (int64_t it = 0;; ++it) {
+        int64_t tile;
+        if (!next_tile(it, tile)) break;
+        tile_read(it);
         int64_t mb;
         int nb;
         bool second;
         const Prob& P = locate(tile, second, mb, nb);
         const bool amn = EPI == EPI_BWD ? second : (AMN != 0);
-        const bool krev = args.k_serp && (it & 1);
+        const bool krev = args.k_serp && ((tile / ncl) & 1);
         const CUtensorMap* mA = second ? &tmA2 : &tmA;
         const CUtensorMap* mB = second ? &tmB2 : &tmB;
         const int32_t m0 = static_cast<int32_t>(mb * C::TILE_M + rank * TC_BM);
@@ -297,7 +336,10 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int64_t tile = cid; tile < num_tiles; tile += ncl) {
+      for (int64_t it = 0;; ++it) {
+        int64_t tile;
+        if (!next_tile(it, tile)) break;
+        tile_read(it);
         int64_t mb_unused;
         int nb_unused;
         bool second;
@@ -339,6 +381,25 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         }
       }
     }
+  } else if (warp == 2) {
+    if (dyn && lane == 0 && leader) {
+      // ------------------------------------------------- tile scheduler
+      for (int64_t it = 0;; ++it) {
+        mbar_wait(sempty + (it & 1), static_cast<uint32_t>(((it >> 1) & 1) ^ 1));
+        int64_t t = it == 0 ? cid : ncl + static_cast<int64_t>(atomicAdd(args.sched, 1u));
+        const int32_t v = t < num_tiles ? static_cast<int32_t>(t) : -1;
+        ring[it & 1] = v;
+        mbar_arrive(sfull + (it & 1));
+        if constexpr (CG == 2) st_cluster_u32_arrive(ring + (it & 1), v, sfull + (it & 1), 1);
+        if (v < 0) break;
+      }
+      // the last scheduler to retire resets the counters for the next launch
+      __threadfence();
+      if (atomicAdd(args.sched + 1, 1u) == static_cast<uint32_t>(ncl - 1)) {
+        atomicExch(args.sched, 0u);
+        atomicExch(args.sched + 1, 0u);
+      }
+    }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
     const int ew = warp - 4;
@@ -353,7 +414,11 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         mbar_arrive(tempty + a);
       }
     };
-    for (int64_t tile = cid; tile < num_tiles; tile += ncl) {
+    for (int64_t it = 0;; ++it) {
+      int64_t tile;
+      if (!next_tile(it, tile)) break;
+      __syncwarp();
+      if (lane == 0) tile_read(it);
       int64_t mb;
       int nb;
       bool second;
@@ -468,11 +533,31 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
               pk[j / 2] = pack_bf16x2(d0, d1);
             }
           }
+          if (args.dz_tma) {
+            // 32 rows x 32 bf16 (64 B) per warp -> smem box, 64-B swizzle
+            // (16-B chunk q of row r at q ^ ((r >> 1) & 3): conflict-free),
+            // one TMA store of whole lines; two buffers per warp.
+            uint8_t* buf = smem + C::STG_OFF + ew * 4096 + (c & 1) * 2048;
+            if (lane == 0) bulk_wait_group_read<1>();
+            __syncwarp();
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
-            st_global_v4_hint(dst + c * 4 + q,
-                              make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]),
-                              st_pol);
+            for (int q = 0; q < 4; ++q)
+              *reinterpret_cast<uint4*>(buf + lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4)) =
+                  make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&tmA2, buf, n0 + c * 32,
+                           static_cast<int32_t>(mb * C::TILE_M + rank * TC_BM + ew * 32), st_pol);
+              bulk_commit_group();
+            }
+          } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              st_global_v4_hint(dst + c * 4 + q,
+                                make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]),
+                                st_pol);
+          }
         }
       } else if (EPI == EPI_ROWS || (EPI == EPI_BWD && !second)) {
         const int64_t orow = row_ok ? static_cast<int64_t>(args.row_idx[row]) : 0;
@@ -595,6 +680,9 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   if constexpr (EPI == EPI_ACC && NB == 2) {
     if (warp >= 4 && lane == 0 && args.acc_red == 2) bulk_wait_group_all();
   }
+  if constexpr (EPI == EPI_DZ) {
+    if (warp >= 4 && lane == 0 && args.dz_tma) bulk_wait_group_all();
+  }
   tc_fence_before();
   __syncwarp();
   if constexpr (CG == 2) cluster_sync(); else __syncthreads();
@@ -641,6 +729,21 @@ static bool make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t 
              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
          CUDA_SUCCESS;
+}
+
+// 2-D bf16 tensor map with a 32 x 32 box and 64-B swizzle: the dZ chunk as a
+// TMA store destination (one epilogue warp's 32 rows x 32 columns).
+static bool make_map_bf16_32(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
+                             uint64_t stride_bytes) {
+  PFN_encodeTiled_t enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {stride_bytes};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 // 2-D fp32 tensor map (dims {inner, outer}, box {box_inner, box_outer},
@@ -731,14 +834,16 @@ static rl_status run_gemm(const CUtensorMap& a, const CUtensorMap& b, const CUte
 // 256-wide tiles (double-buffered TMEM) for the short-K forward/dZ GEMMs.
 template <int AMN, int BMN, int EPI>
 static rl_status run_narrow(const CUtensorMap& a, const CUtensorMap& b, TcArgs t,
-                            int64_t m_extent, int kind, cudaStream_t s) {
+                            int64_t m_extent, int kind, cudaStream_t s,
+                            const CUtensorMap* a2 = nullptr) {
   t.n_tiles = static_cast<int32_t>(ceil_div(t.N, TC_BN));
   t.group_m = env_int("RLHEAD_GROUP_M", 32) / tc_cta_group();
   if (t.group_m < 1) t.group_m = 1;
   const int cg = tc_cta_group();
   const int64_t tiles = ceil_div(m_extent, TC_BM * cg) * t.n_tiles;
-  if (cg == 2) return run_gemm<2, 1, AMN, BMN, EPI>(a, b, a, b, t, tiles, kind, s);
-  return run_gemm<1, 1, AMN, BMN, EPI>(a, b, a, b, t, tiles, kind, s);
+  const CUtensorMap& x2 = a2 ? *a2 : a;
+  if (cg == 2) return run_gemm<2, 1, AMN, BMN, EPI>(a, b, x2, b, t, tiles, kind, s);
+  return run_gemm<1, 1, AMN, BMN, EPI>(a, b, x2, b, t, tiles, kind, s);
 }
 
 // Long-K dH/dW GEMMs: 256 x 512 pair tiles (all 512 TMEM columns), rastered
@@ -778,6 +883,15 @@ static void kind_policy(TcArgs& t, const char* env, int dflt_ab) {
   t.l2_pol_b = ab % 10;
 }
 
+// Dynamic tile scheduler (default; RLHEAD_DYN_SCHED=0 restores the static
+// schedule): one counter slot per GEMM kind. Same-box A/B, Qwen-7B, 1 GPU:
+// +3.8% tokens/s; forward/dZ DRAM reads per micro-batch 7.8/9.2 -> 4.5/4.5 GB
+// (profiles/r1/SUMMARY.md).
+static void use_sched(TcArgs& t, char* ws, const WsLayout& L, int slot) {
+  if (env_int("RLHEAD_DYN_SCHED", 1) == 0) return;
+  t.sched = reinterpret_cast<WsHeader*>(ws + L.off_hdr)->sched[slot];
+}
+
 static TcArgs base_args(const rl_head* hd, const WsLayout& L, char* ws) {
   TcArgs t{};
   t.hdr = reinterpret_cast<const WsHeader*>(ws + L.off_hdr);
@@ -810,6 +924,7 @@ rl_status launch_tc_fwd(const rl_head* hd, const void* weight, const WsLayout& L
   t.pu = reinterpret_cast<float*>(ws + L.off_pu);
   t.zy = reinterpret_cast<float*>(ws + L.off_zy);
   kind_policy(t, "RLHEAD_L2_FWD", -1);
+  use_sched(t, ws, L, 0);
   return run_narrow<0, 0, EPI_LSE>(ma, mb, t, L.Rp, RL_K_GEMM_LSE, s);
 }
 
@@ -841,7 +956,14 @@ rl_status launch_tc_bwd(const rl_head* hd, const void* weight, void* grad_hidden
     t.dz = dz;
     t.ld_dz = L.Vp;
     kind_policy(t, "RLHEAD_L2_DZ", -1);
-    st = run_narrow<0, 0, EPI_DZ>(ma, mb, t, L.Rp, RL_K_GEMM_DZ, s);
+    use_sched(t, ws, L, 1);
+    // TMA stores of the dZ boxes (whole lines) instead of per-row 16-B stores
+    t.dz_tma = env_int("RLHEAD_DZ_TMA", 0);
+    CUtensorMap mdz;
+    if (t.dz_tma &&
+        !make_map_bf16_32(&mdz, dz, V, L.Rp, static_cast<uint64_t>(L.Vp) * 2))
+      return RL_ERR_CUDA;
+    st = run_narrow<0, 0, EPI_DZ>(ma, mb, t, L.Rp, RL_K_GEMM_DZ, s, t.dz_tma ? &mdz : nullptr);
     if (st != RL_OK) return st;
   }
   // N6: dH[T, h] = dZ[T, V] W[V, h]; rows -> grad_hidden[active_idx[r]].
@@ -863,6 +985,7 @@ rl_status launch_tc_bwd(const rl_head* hd, const void* weight, void* grad_hidden
   t6.out_mc = gh_multicast ? 1 : 0;
   t6.row_idx = reinterpret_cast<const int32_t*>(ws + L.off_active);
   kind_policy(t6, "RLHEAD_L2_DH", -1);
+  use_sched(t6, ws, L, 2);
   TcArgs t7 = base_args(hd, L, ws);
   t7.M = V;
   t7.K = L.Rp;
@@ -870,11 +993,14 @@ rl_status launch_tc_bwd(const rl_head* hd, const void* weight, void* grad_hidden
   t7.N = h;
   t7.acc = grad_weight;
   t7.ld_acc = h;
-  // red.add accumulate (default): same-box A/B +1.2% at 16k rows, dW GEMM -8%
-  // (profiles/r1/SUMMARY.md); RLHEAD_DW_RED=0 restores load+add+store
-  t7.acc_red = env_int("RLHEAD_DW_RED", 1);
+  // accumulate: 2 (default) = TMA reduce-add of 32x32 smem boxes (whole L2
+  // lines: dW DRAM reads 30.4 -> 14.9 GB per micro-batch, dW GEMM -9%, +2.1%
+  // tokens/s same-box); 1 = per-row red.global.add.v4; 0 = load+add+store
+  // (profiles/r1/SUMMARY.md)
+  t7.acc_red = env_int("RLHEAD_DW_RED", 2);
   kind_policy(t7, "RLHEAD_L2_DW", -1);
   t7.k_serp = env_int("RLHEAD_DW_SERP", 0);
+  use_sched(t7, ws, L, 3);
   if (dw_rs && dw_rs->world > 1) {
     t7.rs_world = dw_rs->world;
     t7.rs_rank = dw_rs->rank;
@@ -885,6 +1011,7 @@ rl_status launch_tc_bwd(const rl_head* hd, const void* weight, void* grad_hidden
     // one persistent launch over the dH tiles then the dW tiles: the last
     // (partial) wave of dH fills with dW tiles instead of idling.
     TcArgs t = t6;
+    if (t.sched) use_sched(t, ws, L, 4);
     t.n_tiles = static_cast<int32_t>(ceil_div(h, 2 * TC_BN));
     t.group_m = std::max(1, env_int("RLHEAD_GROUP_M_BWD", 1));
     t.M2 = V;

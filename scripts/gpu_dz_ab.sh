@@ -1,0 +1,24 @@
+# TMA dZ stores A/B on top of the new defaults (dynamic scheduler, TMA dW reduce).
+mkdir -p gpurun_out
+timeout -s KILL 1500 python -m pytest -q -x tests/test_gpu_variants.py -k "bit_identical or dz-tma or tma-all or dw-tma or dyn-sched-fused" > gpurun_out/variants_dz.log 2>&1
+echo "variants rc=$?"; tail -3 gpurun_out/variants_dz.log
+CMD="python scripts/probe.py --rows 16384 --reps 1"
+M="gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sector_hit_rate.pct,sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_elapsed,sm__cycles_elapsed.avg.per_second"
+prof() { label=$1; shift
+  env "$@" timeout -s KILL 400 ncu --metrics $M --clock-control none --print-units base -k regex:k_tc_gemm -s 4 -c 4 --csv --log-file gpurun_out/dz_$label.csv $CMD > /dev/null 2>&1
+  echo "== $label rc=$?"
+  python scripts/ncu_metrics_table.py gpurun_out/dz_$label.csv 2>/dev/null | tail -4
+}
+prof new X=1
+prof dztma RLHEAD_DZ_TMA=1
+prof dztma_serp RLHEAD_DZ_TMA=1 RLHEAD_DW_SERP=1
+run() { label=$1; shift
+  env "$@" timeout -s KILL 900 python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-aux > gpurun_out/ab.log 2>&1
+  tail -1 gpurun_out/ab.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$label', d['value'], d['clocks']['sm_mhz'], {k:v['ms_total'] for k,v in d['kernels'].items() if 'gemm' in k})" 2>/dev/null || tail -c 800 gpurun_out/ab.log
+}
+run new X=1
+run dztma RLHEAD_DZ_TMA=1
+run dztma_serp RLHEAD_DZ_TMA=1 RLHEAD_DW_SERP=1
+run new X=1
+run dztma RLHEAD_DZ_TMA=1
+run dztma_serp RLHEAD_DZ_TMA=1 RLHEAD_DW_SERP=1

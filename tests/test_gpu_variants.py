@@ -22,10 +22,19 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
                                  {"RLHEAD_DW_RED": "2"},
                                  {"RLHEAD_L2_DW": "21", "RLHEAD_L2_DH": "21"},
                                  {"RLHEAD_DW_SERP": "1", "RLHEAD_DW_RED": "2"},
-                                 {"RLHEAD_NONPERSIST_DW": "1", "RLHEAD_NONPERSIST_DH": "1"}],
+                                 {"RLHEAD_NONPERSIST_DW": "1", "RLHEAD_NONPERSIST_DH": "1"},
+                                 {"RLHEAD_DYN_SCHED": "1"},
+                                 {"RLHEAD_DYN_SCHED": "1", "RLHEAD_FUSED_BWD": "1",
+                                  "RLHEAD_CTA_GROUP": "2"},
+                                 {"RLHEAD_DYN_SCHED": "1", "RLHEAD_CTA_GROUP": "1"},
+                                 {"RLHEAD_DZ_TMA": "1", "RLHEAD_CTA_GROUP": "1"},
+                                 {"RLHEAD_DZ_TMA": "1", "RLHEAD_DW_RED": "2",
+                                  "RLHEAD_DYN_SCHED": "1"}],
                          ids=["cta1", "cta2-narrow", "cta2-wide-fused", "cta2-unfused-raster",
                               "dw-load-store", "dw-red-fused", "dw-tma-reduce", "l2-hints",
-                              "dw-serpentine", "non-persistent"])
+                              "dw-serpentine", "non-persistent",
+                              "dyn-sched", "dyn-sched-fused", "dyn-sched-cta1",
+                              "dz-tma-cta1", "tma-all-dyn"])
 def test_variant_parity(env):
     import torch
     if not torch.cuda.is_available():
@@ -49,7 +58,7 @@ def test_dw_accumulate_paths_bit_identical(rl):
     from tests.gpu_util import dev_tensors
     from workload import custom_layout
     rng = np.random.default_rng(11)
-    V, h = 3000, 608
+    V, h = 3000, 576
     lay = custom_layout(rng.integers(0, 30, 24), rng.integers(1, 200, 24), np.arange(24) // 4,
                         rng.choice([-5.0, 5.0], 24), vocab=V, num_groups=6)
     d = dev_tensors(lay)
@@ -82,3 +91,60 @@ def test_dw_accumulate_paths_bit_identical(rl):
     assert not torch.equal(out["1"], gw0.cpu())
     assert torch.equal(out["0"], out["1"])
     assert torch.equal(out["2"], out["1"])
+
+
+def test_schedule_and_store_paths_bit_identical(rl):
+    """The dynamic tile scheduler (RLHEAD_DYN_SCHED=1) only changes which CTA
+    pair runs a tile and when, and the TMA dZ stores (RLHEAD_DZ_TMA=1) only
+    how the same bf16 values reach HBM: logp, entropy, dH and dW must be
+    bit-identical to the static schedule with per-row stores, over a multi-
+    wave problem (1.5k forward tiles on 74 pairs, V not a multiple of 32), and
+    the scheduler counters must reset between launches (repeated calls on one
+    workspace give the same result)."""
+    import numpy as np
+    import torch
+    from tests.gpu_util import dev_tensors
+    from workload import custom_layout
+    rng = np.random.default_rng(12)
+    V, h = 32061, 512
+    lay = custom_layout(rng.integers(0, 40, 32), rng.integers(1, 180, 32), np.arange(32) // 8,
+                        rng.choice([-5.0, 5.0], 32), vocab=V, num_groups=4)
+    d = dev_tensors(lay)
+    g = torch.Generator(device="cuda").manual_seed(6)
+    H = torch.randn(lay.num_rows, h, device="cuda", generator=g).to(torch.bfloat16)
+    W = (torch.randn(V, h, device="cuda", generator=g) * (4 / h ** 0.5)).to(torch.bfloat16)
+    head = rl.Head(h, V, "bf16")
+    old = torch.empty(lay.num_rows, device="cuda")
+    rl.rl_logprob_fwd(head, H, W, rl.Batch(d["cu"], d["targets"], d["mask"], d["err"]), old)
+    old += 0.05
+    adv = torch.linspace(-1, 1, lay.num_seqs, device="cuda")
+    ws = rl.Workspace("cuda")
+    variants = [{"RLHEAD_DYN_SCHED": "0", "RLHEAD_DZ_TMA": "0", "RLHEAD_DW_RED": "1"},
+                {"RLHEAD_DYN_SCHED": "1", "RLHEAD_DZ_TMA": "0", "RLHEAD_DW_RED": "1"},
+                {"RLHEAD_DYN_SCHED": "1", "RLHEAD_DZ_TMA": "0", "RLHEAD_DW_RED": "1"},
+                {"RLHEAD_DYN_SCHED": "0", "RLHEAD_DZ_TMA": "1", "RLHEAD_DW_RED": "2"},
+                {"RLHEAD_DYN_SCHED": "1", "RLHEAD_DZ_TMA": "1", "RLHEAD_DW_RED": "2"}]
+    res = []
+    saved = {k: os.environ.get(k) for k in variants[0]}
+    try:
+        for env in variants:
+            os.environ.update(env)
+            logp = torch.empty(lay.num_rows, device="cuda")
+            ent = torch.empty(lay.num_rows, device="cuda")
+            gh = torch.empty_like(H)
+            gw = torch.zeros(V, h, device="cuda")
+            b = rl.Batch(d["cu"], d["targets"], d["mask"], d["err"])
+            rl.rl_policy_loss_fwd_bwd(head, H, W, b, old, adv, rl.LossParams(), logp, gh, gw,
+                                      entropy=ent, ws=ws)
+            torch.cuda.synchronize()
+            res.append([x.cpu() for x in (logp, ent, gh, gw)])
+    finally:
+        for k, v in saved.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    for env, other in zip(variants[1:], res[1:]):
+        for name, a, b in zip(("logp", "entropy", "dH", "dW"), res[0], other):
+            assert torch.equal(a, b), (env, name)
+    assert float(res[0][3].abs().max()) > 0

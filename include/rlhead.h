@@ -23,7 +23,11 @@
  *     are OR-ed into the optional device word `err_flags` (RL_DEVERR_*) and
  *     the offending rows/sequences are treated as inactive; no host sync.
  *   - Re-entrant: concurrent calls on different streams are legal when their
- *     outputs and workspaces are disjoint.
+ *     outputs and workspaces are disjoint. The workspace also holds the
+ *     tensor-core GEMMs' tile-scheduler counters; every launch
+ *     leaves them at zero (and the bookkeeping pass zeroes them), so a
+ *     workspace carries no state from one call to the next, but one
+ *     workspace must never be used by two calls in flight at once.
  */
 #ifndef RLHEAD_H
 #define RLHEAD_H

@@ -40,9 +40,10 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--config", default="qwen7b")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--mb-rows", type=int, default=32768,
-                   help="rows per micro-batch (same-box A/B with the v5 kernels: 32k +0.35%% "
-                        "over 16k, 8k -3.4%%; profiles/r1/SUMMARY.md)")
+    p.add_argument("--mb-rows", type=int, default=16384,
+                   help="rows per micro-batch (same-box A/B with the v5 kernels: 32k within "
+                        "0.35%% of 16k but 1.8x the dW DRAM bytes per token, 8k -3.4%%; "
+                        "profiles/r1/SUMMARY.md)")
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--max-mb", type=int, default=0, help="debug: first micro-batches only")
     p.add_argument("--no-e2e", action="store_true")

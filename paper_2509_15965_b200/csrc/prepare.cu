@@ -43,6 +43,10 @@ __device__ __forceinline__ int32_t upper_bound_i32(const int32_t* __restrict__ c
   return lo;
 }
 
+// Rows per thread: ROWS_PT consecutive rows, so the row -> sequence map needs
+// one binary search of cu_seqlens per thread, then a forward walk.
+constexpr int ROWS_PT = PREP_ROWS / PREP_THREADS;
+
 __global__ void __launch_bounds__(PREP_THREADS)
 k_flags(const int32_t* __restrict__ cu, int32_t S, int64_t R, const int32_t* __restrict__ targets,
         const uint8_t* __restrict__ mask, int32_t V, const WsHeader* __restrict__ hdr,
@@ -50,21 +54,24 @@ k_flags(const int32_t* __restrict__ cu, int32_t S, int64_t R, const int32_t* __r
         float* zero0, float* zero1, float* zero2, int32_t* err) {
   const int bad = hdr->bad_cu;
   int cnt = 0, terr = 0;
+  const int64_t t0 = static_cast<int64_t>(blockIdx.x) * PREP_ROWS + threadIdx.x * ROWS_PT;
+  // last sequence s with cu[s] <= t0 (empty sequences skipped), as the binary
+  // search below each row would give
+  int32_t s = (!bad && t0 < R) ? upper_bound_i32(cu, S + 1, t0) - 1 : -1;
 #pragma unroll
-  for (int j = 0; j < PREP_ROWS / PREP_THREADS; ++j) {
-    const int64_t t = static_cast<int64_t>(blockIdx.x) * PREP_ROWS + j * PREP_THREADS + threadIdx.x;
+  for (int j = 0; j < ROWS_PT; ++j) {
+    const int64_t t = t0 + j;
     if (t >= R) break;
-    int32_t s = -1;
     uint8_t a = 0;
     if (!bad) {
-      s = upper_bound_i32(cu, S + 1, t) - 1;
+      while (s < S && static_cast<int64_t>(__ldg(cu + s + 1)) <= t) ++s;
       if (mask[t]) {
         const int32_t y = targets[t];
         if (y >= 0 && y < V) a = 1; else terr = 1;
       }
     }
     act[t] = a;
-    row_seq[t] = s;
+    row_seq[t] = bad ? -1 : s;
     cnt += a;
     if (!a) {
       if (zero0) zero0[t] = 0.f;
@@ -122,29 +129,36 @@ k_compact(int64_t R, const uint8_t* __restrict__ act, const int32_t* __restrict_
           const int32_t* __restrict__ targets, const int64_t* __restrict__ blk_off,
           int32_t* __restrict__ active_idx, int32_t* __restrict__ tgt_c,
           int32_t* __restrict__ seq_c) {
+  // Thread = ROWS_PT consecutive rows (packed order = thread order, then row):
+  // exclusive offset = block offset + warps before + lanes before (shuffle scan).
   __shared__ int wcnt[PREP_THREADS / 32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int64_t base = blk_off[blockIdx.x];
-  for (int j = 0; j < PREP_ROWS / PREP_THREADS; ++j) {
-    const int64_t t = static_cast<int64_t>(blockIdx.x) * PREP_ROWS + j * PREP_THREADS + threadIdx.x;
-    const int a = (t < R) ? act[t] : 0;
-    const unsigned bal = __ballot_sync(0xffffffffu, a);
-    const int pre = __popc(bal & ((1u << lane) - 1u));
-    if (lane == 0) wcnt[warp] = __popc(bal);
-    __syncthreads();
-    int woff = 0, tot = 0;
-    for (int w = 0; w < PREP_THREADS / 32; ++w) {
-      woff += (w < warp) ? wcnt[w] : 0;
-      tot += wcnt[w];
-    }
-    if (a) {
-      const int64_t o = base + woff + pre;
+  const int64_t t0 = static_cast<int64_t>(blockIdx.x) * PREP_ROWS + threadIdx.x * ROWS_PT;
+  uint32_t bits = 0;
+#pragma unroll
+  for (int j = 0; j < ROWS_PT; ++j)
+    if (t0 + j < R && act[t0 + j]) bits |= 1u << j;
+  const int c = __popc(bits);
+  int incl = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) wcnt[warp] = incl;
+  __syncthreads();
+  int woff = 0;
+  for (int w = 0; w < warp; ++w) woff += wcnt[w];
+  int64_t o = blk_off[blockIdx.x] + woff + (incl - c);
+#pragma unroll
+  for (int j = 0; j < ROWS_PT; ++j) {
+    if (bits & (1u << j)) {
+      const int64_t t = t0 + j;
       active_idx[o] = static_cast<int32_t>(t);
       tgt_c[o] = targets[t];
       seq_c[o] = row_seq[t];
+      ++o;
     }
-    base += tot;
-    __syncthreads();
   }
 }
 

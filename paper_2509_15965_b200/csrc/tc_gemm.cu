@@ -1038,7 +1038,8 @@ rl_status launch_tc_bwd(const rl_head* hd, const void* weight, void* grad_hidden
   if ((st = run_wide<0, 1, EPI_ROWS>(ma6, mb6, t6, L.Rp, RL_K_GEMM_DH, s)) != RL_OK) return st;
   CUtensorMap macc;
   if (t7.acc_red == 2) {
-    if (t7.rs_world > 0) t7.acc_red = 1;  // reduce-scatter epilogue: plain stores
+    // TMA needs a 16-B aligned base; the reduce-scatter epilogue stores plainly
+    if (t7.rs_world > 0 || (reinterpret_cast<uintptr_t>(grad_weight) & 15) != 0) t7.acc_red = 1;
     else if (!make_map_f32(&macc, grad_weight, h, V, static_cast<uint64_t>(h) * 4, 32, 32))
       return RL_ERR_CUDA;
   }

@@ -989,6 +989,8 @@ rl_status launch_tc_bwd(const rl_head* hd, const void* weight, void* grad_hidden
   t6.out_mc = gh_multicast ? 1 : 0;
   t6.row_idx = reinterpret_cast<const int32_t*>(ws + L.off_active);
   kind_policy(t6, "RLHEAD_L2_DH", -1);
+  // serpentine K for dH measured neutral (~6 waves per micro-batch): off
+  t6.k_serp = env_int("RLHEAD_DH_SERP", 0);
   use_sched(t6, ws, L, 2);
   TcArgs t7 = base_args(hd, L, ws);
   t7.M = V;

@@ -100,11 +100,13 @@ def _worker(rank, world, port, out_dir):
     dist.destroy_process_group()
 
 
-def test_gloo_world2_matches_whole_batch(tmp_path):
+@pytest.mark.parametrize("world", [2, 4])
+def test_gloo_world_matches_whole_batch(tmp_path, world):
+    """world 4 on the tiny config (2 prompt groups) leaves two ranks with no
+    sequences: they must still join every collective with zero contributions."""
     import torch.multiprocessing as mp
 
     from paper_2509_15965_b200 import rlhead as R
-    world = 2
     mp.start_processes(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world,
                        join=True, start_method="spawn")
     cfg = CONFIGS["tiny"]

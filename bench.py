@@ -48,7 +48,10 @@ def parse():
     p.add_argument("--max-mb", type=int, default=0, help="debug: first micro-batches only")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--cpu-sample-tokens", type=int, default=512)
+    p.add_argument("--cpu-sample-tokens", type=int, default=512,
+                   help="masked tokens per --impl reference step")
+    p.add_argument("--cpu-baseline-tokens", type=int, default=1536,
+                   help="masked tokens of the cpu_baseline leg (about 10-30 s of oracle work)")
     p.add_argument("--collective", default="symm", choices=["symm", "nccl"],
                    help="N>1 dW reduction: reduce-scatter fused into the last dW GEMM epilogue "
                         "+ NVLink all-gather (symm), or NCCL all-reduce")
@@ -316,7 +319,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(cfg, layout, args.seed, args.cpu_sample_tokens)
+        cpu = cpu_baseline(cfg, layout, args.seed, args.cpu_baseline_tokens)
 
     if rank == 0:
         line = {

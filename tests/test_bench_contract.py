@@ -45,3 +45,18 @@ def test_reference_arm_under_torchrun_rank0_only():
     assert out.returncode == 0, out.stderr[-2000:]
     lines = [x for x in out.stdout.splitlines() if x.startswith("{")]
     assert len(lines) == 1 and json.loads(lines[0])["n_gpus"] == 2
+
+
+def test_cpu_baseline_leg_bounded_oracle_sample():
+    """The N=1 cpu_baseline leg times the oracle on the first `tokens` masked rows
+    of sequence 0: the reported sample size is the active-row count, bounded by
+    the request, and value = tokens / seconds."""
+    sys.path.insert(0, ROOT)
+    import bench
+    from workload import CONFIGS, make_layout
+    cfg = CONFIGS["tiny"]
+    cb = bench.cpu_baseline(cfg, make_layout(cfg, seed=0), 0, 8)
+    assert cb["kind"] == "oracle" and cb["unit"] == "tokens/s" and cb["cores"] >= 1
+    n = int(cb["sample"].split()[0])
+    assert 1 <= n <= 8
+    assert abs(cb["value"] - n / cb["seconds"]) <= 1e-9 * cb["value"]

@@ -52,6 +52,8 @@ def parse():
                    help="masked tokens per --impl reference step")
     p.add_argument("--cpu-baseline-tokens", type=int, default=1536,
                    help="masked tokens of the cpu_baseline leg (about 10-30 s of oracle work)")
+    p.add_argument("--cpu-1t-tokens", type=int, default=64,
+                   help="masked tokens of the cpu_baseline leg's 1-thread run (SURVEY M.7)")
     p.add_argument("--collective", default="symm", choices=["symm", "nccl"],
                    help="N>1 dW reduction: reduce-scatter fused into the last dW GEMM epilogue "
                         "+ NVLink all-gather (symm), or NCCL all-reduce")
@@ -132,34 +134,102 @@ def dist_env():
     return rank, world, local
 
 
-def cpu_baseline(cfg, layout, seed, tokens):
-    """The oracle as it stands on this host, on a bounded sample: the first
-    `tokens` response rows of sequence 0 (with its prompt rows), fwd+bwd."""
+_W64 = {}
+
+
+def _oracle_weight(cfg, seed):
+    """The config's W as float64 (exact bf16/fp32 values), built once outside
+    any timed region (the conversion is a fixed cost that does not scale with
+    the sampled token count)."""
     import torch
 
-    import oracle
-    from workload import make_tensors_host, sub_layout
+    from workload import make_tensors_torch
+    key = (cfg.name, seed)
+    if key not in _W64:
+        _, W = make_tensors_torch(cfg, 0, seed=seed, hidden=False)
+        _W64[key] = W.to(torch.float64).numpy()
+    return _W64[key]
+
+
+def _blas_threads():
     try:
         from threadpoolctl import threadpool_info
-        blas = max([i.get("num_threads", 0) for i in threadpool_info()] or [0])
+        return max([i.get("num_threads", 0) for i in threadpool_info()] or [0])
     except Exception:
-        blas = 0
+        return 0
+
+
+def cpu_baseline(cfg, layout, seed, tokens, threads=None):
+    """The oracle as it stands on this host, on a bounded sample: the first
+    `tokens` response rows of sequence 0 (with its prompt rows), fwd+bwd.
+    W is converted to float64 before the clock starts; threads=k limits the
+    BLAS pool to k threads for the timed call."""
+    import contextlib
+
+    import oracle
+    from workload import make_tensors_torch, sub_layout
     sub, _ = sub_layout(layout, [0])
     P = int(sub.prompt_len[0]) if sub.prompt_len is not None else 0
     R = min(sub.num_rows, P + tokens)
     cu = np.array([0, R], dtype=np.int32)
     mask, targets = sub.mask[:R], sub.targets[:R]
-    H, W = make_tensors_host(cfg, R, seed=seed)
+    H, _ = make_tensors_torch(cfg, R, seed=seed, weight=False)
+    W64 = _oracle_weight(cfg, seed)
     old = np.zeros(R)
     adv = np.array([1.0])
-    t0 = time.perf_counter()
-    out = oracle.policy_loss_fwd_bwd(H, W, cu, mask, targets, old, adv)
-    dt = time.perf_counter() - t0
-    del torch
+    lim = contextlib.nullcontext()
+    if threads is not None:
+        from threadpoolctl import threadpool_limits
+        lim = threadpool_limits(limits=threads)
+    with lim:
+        blas = _blas_threads()
+        t0 = time.perf_counter()
+        out = oracle.policy_loss_fwd_bwd(H, W64, cu, mask, targets, old, adv)
+        dt = time.perf_counter() - t0
     n = int(out["n_active"])
-    return {"value": n / dt, "unit": "tokens/s", "cores": os.cpu_count(), "blas_threads": blas,
-            "kind": "oracle", "seconds": dt,
+    return {"value": n / dt, "unit": "tokens/s", "cores": blas or os.cpu_count(),
+            "host_cpus": os.cpu_count(), "blas_threads": blas, "kind": "oracle", "seconds": dt,
             "sample": f"{n} masked tokens of sequence 0 ({cfg.name}, fwd+bwd incl. dW [V,h] fp64)"}
+
+
+def cpu_tiny_end_to_end(seed=0):
+    """the tiny config (BJ configs[0]) through the whole oracle path
+    end to end: bookkeeping, GRPO advantages, fwd+bwd of the full batch."""
+    import oracle
+    from workload import CONFIGS, make_layout, make_tensors_host
+    cfg = CONFIGS["tiny"]
+    lay = make_layout(cfg, seed=seed)
+    H, W = make_tensors_host(cfg, lay.num_rows, seed=seed)
+    t0 = time.perf_counter()
+    adv, _ = oracle.grpo_advantage(lay.rewards, lay.group_of_seq, lay.num_groups)
+    out = oracle.policy_loss_fwd_bwd(H, W, lay.cu_seqlens, lay.mask, lay.targets,
+                                     np.zeros(lay.num_rows), adv)
+    dt = time.perf_counter() - t0
+    return {"workload": "tiny (2 prompts x G=4, h=64, V=1000), whole batch",
+            "tokens": int(out["n_active"]), "seconds": round(dt, 4),
+            "value": round(int(out["n_active"]) / dt, 1), "unit": "tokens/s"}
+
+
+def cpu_baseline_m7(cfg, layout, seed, tokens, tokens_1t, tokens_global):
+    """all host threads on `tokens`, 1 thread on `tokens_1t`,
+    the tiny config end to end, and the full config's time extrapolated from
+    the all-thread per-token rate (labelled as such)."""
+    cb = cpu_baseline(cfg, layout, seed, tokens)
+    one = cpu_baseline(cfg, layout, seed, tokens_1t, threads=1)
+    cb["one_thread"] = {"value": one["value"], "seconds": round(one["seconds"], 3),
+                        "sample": one["sample"], "cores": 1}
+    cb["tiny_end_to_end"] = cpu_tiny_end_to_end(seed)
+    cb["full_config_extrapolated"] = {
+        "tokens": int(tokens_global), "seconds": round(tokens_global / cb["value"], 1),
+        "hours": round(tokens_global / cb["value"] / 3600.0, 2),
+        "note": "extrapolated: full mini-batch tokens / the all-thread sample's tokens/s "
+                "(not run)"}
+    return cb
+
+
+def workload_name(cfg):
+    return (f"{cfg.name} head (h={cfg.hidden}, V={cfg.vocab}), {cfg.prompts} prompts x "
+            f"G={cfg.group}, responses <= {cfg.lmax}")
 
 
 def run_reference(args, cfg):
@@ -182,12 +252,32 @@ def run_reference(args, cfg):
             "ms_per_step": 1000.0 * statistics.median([x["seconds"] for x in vals]),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
-            "config": {"workload": cfg.name, "sample": cb["sample"]},
+            "config": {"workload": workload_name(cfg), "sample": cb["sample"]},
+            "gpus_used": 0, "host_only": "the CPU float64 oracle on the host cores",
             "cpu_baseline": cb,
             "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def _free_port():
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def relaunch_under_torchrun(args):
+    """`python bench.py --gpus N` (N > 1) without a torchrun environment:
+    re-exec as one rank per GPU (the driver's own launch form) and pass the
+    ranks' output and exit code through."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(_free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    print(f"[bench] --gpus {args.gpus} without WORLD_SIZE: relaunching under torchrun",
+          file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
 
 
 def main():
@@ -196,6 +286,13 @@ def main():
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         return run_reference(args, cfg)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch_under_torchrun(args)
+    if int(os.environ.get("WORLD_SIZE", "1")) != args.gpus:
+        print(f"[bench] --gpus {args.gpus} but WORLD_SIZE={os.environ.get('WORLD_SIZE')}: "
+              "launch one rank per GPU (torchrun --nproc-per-node N ... --gpus N)",
+              file=sys.stderr, flush=True)
+        return 2
 
     import torch
     import torch.distributed as dist
@@ -253,12 +350,17 @@ def main():
         torch.cuda.synchronize()
 
     # ------------------------------------------------------ device-timed run
-    for _ in range(args.warmup):
+    for i in range(args.warmup):
+        if i == args.warmup - 1:
+            nw = rl.rl_launch_count()
         step.run(H, old, gh)
+    per_step_launches = rl.rl_launch_count() - nw
     barrier()
     clk = Clocks(local)
     clk.start()
-    tr = rl.Trace(1 << 17).start()
+    # every launch of the timed steps is traced (the roofline's time is the sum
+    # over ALL dominant-kernel launches; checked against rl_launch_count below)
+    tr = rl.Trace(per_step_launches * args.steps + 4096).start()
     n0 = rl.rl_launch_count()
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     e0, e1 = evs[0], evs[-1]
@@ -271,6 +373,8 @@ def main():
     launches = rl.rl_launch_count() - n0
     tr.stop()
     clocks = clk.stop()
+    if len(tr.kinds) != launches:
+        raise RuntimeError(f"trace holds {len(tr.kinds)} of {launches} launches: roofline invalid")
     ms = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(ms, op=dist.ReduceOp.MAX)
@@ -319,18 +423,19 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(cfg, layout, args.seed, args.cpu_baseline_tokens)
+        cpu = cpu_baseline_m7(cfg, layout, args.seed, args.cpu_baseline_tokens,
+                              args.cpu_1t_tokens, tokens_global)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 1), "unit": "tokens/s", "n_gpus": world,
+            "gpus_active": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3),
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": cfg.dtype,
             "step_ms_rank0": {"median": round(statistics.median(per_step), 3),
                               "min": round(min(per_step), 3), "max": round(max(per_step), 3)},
             "data": "synthetic",
-            "config": {"workload": f"{cfg.name} head (h={cfg.hidden}, V={cfg.vocab}), "
-                                   f"{cfg.prompts} prompts x G={cfg.group}, responses <= {cfg.lmax}",
+            "config": {"workload": workload_name(cfg),
                        "global_batch_tokens": tokens_global, "micro_batch_rows": args.mb_rows,
                        "micro_batches_per_rank": len(db.mbs), "parallelism": f"dp{world}",
                        "dw_collective": collective,
@@ -422,11 +527,14 @@ def run_aux(rl, head, H, W, db, mine, step, kinds, tokens_local, tokens_global, 
 
 
 def run_e2e(args, rl, step, db, mine, H, old, gh, dev, world, tokens_global):
-    """Same metric through the public API with HOST inputs: every step copies
-    its inputs from pinned host memory (hidden streamed per micro-batch on a
-    copy stream, double-buffered, the next step's first micro-batches
-    prefetched under this step's last ones) and reads the loss statistics
-    back."""
+    """Same metric through the public API with HOST buffers on both sides.
+    Every step copies its inputs from pinned host memory (hidden streamed per
+    micro-batch on a copy stream, double-buffered, the next step's first
+    micro-batches prefetched under this step's last ones) and reads its
+    results back on a second copy stream: each micro-batch's log-probs (the
+    inference worker's output) as soon as its call is enqueued, this
+    rank's slab of the reduced dW (the rows a sharded optimizer owns) and the
+    loss statistics at the end of the step."""
     import torch
     import torch.distributed as dist
     R = mine.num_rows
@@ -440,12 +548,21 @@ def run_e2e(args, rl, step, db, mine, H, old, gh, dev, world, tokens_global):
     max_mb = gh.shape[0]
     bufs = [torch.empty(max_mb, H.shape[1], dtype=H.dtype, device=dev) for _ in range(2)]
     copy_s = torch.cuda.Stream(device=dev)
+    d2h_s = torch.cuda.Stream(device=dev)
     ready = [torch.cuda.Event() for _ in range(2)]
     freed = [torch.cuda.Event() for _ in range(2)]
     comp = torch.cuda.current_stream()
     stats_host = torch.empty(rl.rlhead.STATS_BYTES, dtype=torch.uint8, pin_memory=True)
+    logp_host = torch.empty(max(R, 1), dtype=torch.float32, pin_memory=True)
+    rank = dist.get_rank() if world > 1 else 0
+    V = step.grad_w.shape[0]
+    slab = -(-V // world)
+    v0, v1 = min(rank * slab, V), min((rank + 1) * slab, V)
+    dw_host = torch.empty((v1 - v0, step.grad_w.shape[1]), dtype=torch.float32, pin_memory=True)
     h2d = sum(v.numel() * v.element_size() for v in host_small.values()) + \
         sum((r1 - r0) * H.shape[1] * H.element_size() for _, _, r0, r1, _ in db.mbs)
+    d2h = 4 * sum(r1 - r0 for _, _, r0, r1, _ in db.mbs) + dw_host.numel() * 4 + \
+        rl.rlhead.STATS_BYTES
 
     n_mb = len(db.mbs)
     # micro-batches are numbered c = step * n_mb + i across the steps of one run
@@ -470,6 +587,10 @@ def run_e2e(args, rl, step, db, mine, H, old, gh, dev, world, tokens_global):
     def after_mb(i):
         c = state["base"] + i
         freed[c % 2].record(comp)
+        _, _, r0, r1, _ = db.mbs[i]
+        with torch.cuda.stream(d2h_s):       # this micro-batch's log-probs -> host
+            d2h_s.wait_event(freed[c % 2])
+            logp_host[r0:r1].copy_(step.logp[r0:r1], non_blocking=True)
         if c + 2 < state["total"]:
             issue_copy(c + 2)
 
@@ -488,7 +609,13 @@ def run_e2e(args, rl, step, db, mine, H, old, gh, dev, world, tokens_global):
         for c in range(state["issued"], min(b + 2, state["total"])):
             issue_copy(c)            # not prefetched by the previous step
         step.run(None, dev_small["old"], gh, hidden_for_mb=hidden_for_mb, after_mb=after_mb)
-        stats_host.copy_(step.stats, non_blocking=True)
+        done = torch.cuda.Event()
+        done.record(comp)
+        with torch.cuda.stream(d2h_s):       # reduced dW slab + stats -> host
+            d2h_s.wait_event(done)
+            dw_host.copy_(step.grad_w[v0:v1], non_blocking=True)
+            stats_host.copy_(step.stats, non_blocking=True)
+        comp.wait_stream(d2h_s)              # the next step zeroes dW/stats after the read
         state["base"] = b + n_mb
 
     def run(k):
@@ -513,9 +640,15 @@ def run_e2e(args, rl, step, db, mine, H, old, gh, dev, world, tokens_global):
     if world > 1:
         dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     v = tokens_global / (float(ms.item()) / 1e3)
+    # the host copies are the step's results: same values as the device run
+    ok = bool(torch.equal(logp_host[:R], step.logp[:R].cpu())) and \
+        bool(torch.equal(dw_host, step.grad_w[v0:v1].cpu()))
     del host_H
     return {"value": round(v, 1), "unit": "tokens/s", "h2d_bytes_per_step": int(h2d),
-            "d2h_bytes_per_step": int(rl.rlhead.STATS_BYTES), "ms_per_step": round(float(ms.item()), 3)}
+            "d2h_bytes_per_step": int(d2h), "ms_per_step": round(float(ms.item()), 3),
+            "d2h": "per micro-batch logp [rows] fp32 + this rank's dW slab "
+                   f"[{v1 - v0}, {step.grad_w.shape[1]}] fp32 + 72 B stats (bytes per rank)",
+            "host_results_match_device": ok}
 
 
 if __name__ == "__main__":

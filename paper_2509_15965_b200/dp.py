@@ -182,7 +182,8 @@ class PolicyLossStep:
     """One GRPO mini-batch step of the head on this rank."""
 
     def __init__(self, head, weight, db: DeviceBatch, params=None, group=None,
-                 advantage: str = "grpo", collective: str = "nccl", split_groups: bool = False):
+                 advantage: str = "grpo", collective: str = "nccl", split_groups: bool = False,
+                 want_entropy: bool = False):
         import torch
         from . import rlhead as R
         self.R = R
@@ -210,6 +211,8 @@ class PolicyLossStep:
                                       device=dev)
         self.stats = R.new_stats(dev)
         self.logp = torch.empty(max(db.num_rows, 1), dtype=torch.float32, device=dev)
+        self.entropy = (torch.empty(max(db.num_rows, 1), dtype=torch.float32, device=dev)
+                        if want_entropy else None)
         self.ws = R.Workspace(dev)
         self.ws_prep = R.Workspace(dev)
 
@@ -271,8 +274,9 @@ class PolicyLossStep:
             self.params.dw_reduce_scatter = (self.peer_group if self.symm is not None and i == last
                                              else None)
             R.rl_policy_loss_fwd_bwd(self.head, hs, self.W, b, old_logp[r0:r1], self.adv[s0:s1],
-                                     self.params, self.logp[r0:r1], gh,
-                                     self.grad_w, stats=self.stats, ws=self.ws)
+                                     self.params, self.logp[r0:r1], gh, self.grad_w,
+                                     entropy=None if self.entropy is None else self.entropy[r0:r1],
+                                     stats=self.stats, ws=self.ws)
             if after_mb:
                 after_mb(i)
         self.params.dw_reduce_scatter = None
@@ -340,6 +344,11 @@ class StreamingPolicyLoss:
         """last=True on this rank's final micro-batch of the global batch lets its
         dW epilogue run the fused reduce-scatter (collective="symm")."""
         R = self.R
+        if self.sent:
+            # the fused reduce-scatter already shipped this rank's partial: a
+            # later micro-batch's dW would never reach the reduction
+            raise RuntimeError("feed() after the micro-batch marked last=True; call begin() "
+                               "to start the next global batch")
         R.rl_batch_prepare(self.head, batch, n_accum=self.n_tokens, ws=self.ws_prep)
         fuse = self.symm is not None and last and not self.sent
         self.params.dw_reduce_scatter = self.peer_group if fuse else None

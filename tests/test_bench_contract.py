@@ -60,3 +60,30 @@ def test_cpu_baseline_leg_bounded_oracle_sample():
     n = int(cb["sample"].split()[0])
     assert 1 <= n <= 8
     assert abs(cb["value"] - n / cb["seconds"]) <= 1e-9 * cb["value"]
+
+
+def test_gpu_arm_refuses_world_mismatch():
+    """--gpus N must equal the torchrun world: a mismatch exits 2 before any
+    device work (without WORLD_SIZE, --gpus N > 1 relaunches under torchrun)."""
+    env = dict(os.environ, WORLD_SIZE="3", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2",
+                          "--config", "tiny"], capture_output=True, text=True, timeout=300,
+                         cwd=ROOT, env=env)
+    assert out.returncode == 2, (out.returncode, out.stderr[-2000:])
+    assert "WORLD_SIZE=3" in out.stderr
+
+
+def test_cpu_baseline_m7_pieces():
+    """all-thread sample, 1-thread sample, tiny end to end, and the
+    full config's extrapolated time, labelled as extrapolated."""
+    sys.path.insert(0, ROOT)
+    import bench
+    from workload import CONFIGS, make_layout
+    cfg = CONFIGS["tiny"]
+    lay = make_layout(cfg, seed=0)
+    cb = bench.cpu_baseline_m7(cfg, lay, 0, 8, 4, lay.num_tokens)
+    assert cb["one_thread"]["cores"] == 1 and cb["one_thread"]["value"] > 0
+    assert cb["tiny_end_to_end"]["tokens"] == lay.num_tokens
+    ex = cb["full_config_extrapolated"]
+    assert "extrapolated" in ex["note"]
+    assert abs(ex["seconds"] - lay.num_tokens / cb["value"]) <= 0.06

@@ -1,19 +1,179 @@
-"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py
-times (one 65,536-row micro-batch of the real layout through
-rl_policy_loss_fwd_bwd), on outputs the oracle can compute one by one:
-sampled rows' logp / entropy / dL/dH, plus properties that hold at any size
-(P14 column sums of dW, micro-batch linearity of dW, masked rows exactly 0)."""
+"""Parity at BASELINE.json's full head sizes, in the launch configuration
+bench.py times (PolicyLossStep with 16,384-row micro-batches: the same
+driver, kernels, tile shapes and dW accumulation path).
+
+* test_fullsize_oracle_subbatch: a sub-batch of WHOLE sequences of the real
+  layout run through the bench's driver and through
+  the CPU float64 oracle on the same values: every row's logp and entropy
+  (<= 2e-3), loss_sum / ratio_sum / entropy_sum (rel 1e-2), tokens and both
+  clip counts (exact; the guard band keeps fp32 and fp64 on the same side
+  of 1 +- eps), advantages (1e-5), dH and dW (rel_fro and max_rel <= 1e-2).
+  At the 7B/32B heads the dW GEMM has K ~ 4k rows (16 k-blocks of 256) and
+  56 waves, so odd (serpentine, K walked backwards) waves are covered.
+  Token-level mean over the sub-batch's N, micro-batch = fwd/bwd
+  unit.
+* test_fullsize_sampled_rows: the first 16k-row micro-batch of each real
+  layout, sampled rows' logp / entropy / dL/dH vs the oracle, plus the P14
+  column-sum bound on dW and exact zeros on masked rows.
+* test_fullsize_dw_linearity: dW of a micro-batch == dW of its halves.
+"""
 import numpy as np
 import pytest
 
 import oracle
 from paper_2509_15965_b200.dp import pack_micro_batches
-from tests.gpu_util import max_rel, rel_fro
+from tests.gpu_util import guarded_old_logp, max_rel, rel_fro
 from workload import CONFIGS, make_layout, make_tensors_torch, ratio_noise, sub_layout
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
-MB_ROWS = 65536
+MB_ROWS = 16384          # bench.py --mb-rows default
+
+
+def _seq_tokens(lay):
+    cu = lay.cu_seqlens.astype(np.int64)
+    return np.add.reduceat(lay.mask.astype(np.int64), cu[:-1])
+
+
+def _whole_seq_subbatch(lay, target):
+    """Whole sequences of the real layout with >= `target` response tokens:
+    the two shortest of the forced all-correct group 0 (zero variance ->
+    A = 0 exactly, rows with no gradient) plus the shortest sequences of the
+    mixed-reward group that reaches `target` with the fewest tokens."""
+    tok = _seq_tokens(lay)
+    gos = lay.group_of_seq
+    g0 = np.flatnonzero(gos == 0)
+    sel = list(g0[np.argsort(tok[g0], kind="stable")][:2])
+    t0 = int(tok[sel].sum())
+    best = None
+    for g in range(2, lay.num_groups):
+        m = np.flatnonzero(gos == g)
+        acc, s = [], t0
+        for i in m[np.argsort(tok[m], kind="stable")]:
+            acc.append(int(i))
+            s += int(tok[i])
+            if s >= target and len(set(lay.rewards[acc].tolist())) == 2:
+                break
+        if s >= target and len(set(lay.rewards[acc].tolist())) == 2 and \
+                (best is None or s < best[0]):
+            best = (s, acc)
+    return np.array(sorted(sel + best[1]))
+
+
+def _smallest_groups(lay, k):
+    tok = _seq_tokens(lay)
+    g_tok = np.bincount(lay.group_of_seq, weights=tok, minlength=lay.num_groups)
+    groups = np.argsort(g_tok, kind="stable")[:k]
+    return np.flatnonzero(np.isin(lay.group_of_seq, groups))
+
+
+def _subbatch(name):
+    cfg = CONFIGS[name]
+    lay = make_layout(cfg, seed=0)
+    if name == "qwen1.5b":
+        seqs = _smallest_groups(lay, 2)          # two whole prompt groups
+    elif name == "openvla":
+        seqs = np.flatnonzero(lay.group_of_seq == 5)   # one whole group of 8 envs
+    else:
+        seqs = _whole_seq_subbatch(lay, 4096)
+    sub, _ = sub_layout(lay, seqs)
+    return cfg, sub
+
+
+def _chunked_cmp(gpu, ref, chunk=8192):
+    """(rel_fro, max_rel) of a device fp32/bf16 matrix vs a float64 host
+    matrix, streamed in row chunks (the 32B dW is 3.1 GB fp32 / 6.2 GB fp64)."""
+    import torch
+    num = den = 0.0
+    dmax = rmax = 0.0
+    for r0 in range(0, ref.shape[0], chunk):
+        a = gpu[r0:r0 + chunk].to(torch.float64).cpu().numpy()
+        b = ref[r0:r0 + chunk]
+        d = a - b
+        num += float(np.sum(d * d))
+        den += float(np.sum(b * b))
+        dmax = max(dmax, float(np.abs(d).max()))
+        rmax = max(rmax, float(np.abs(b).max()))
+    return (num / den) ** 0.5 if den > 0 else num ** 0.5, dmax / rmax if rmax > 0 else dmax
+
+
+_ORACLE_CACHE = {}
+
+
+def _oracle_case(name):
+    """(cfg, sub-layout, H, W on cuda, old, oracle result) -- the oracle runs
+    once per config (minutes of float64 work at the 32B head)."""
+    import torch
+    if name in _ORACLE_CACHE:
+        return _ORACLE_CACHE[name]
+    cfg, sub = _subbatch(name)
+    H, W = make_tensors_torch(cfg, sub.num_rows, seed=3, device="cuda")
+    Hh, Wh = H.cpu(), W.cpu()
+    W64 = Wh.to(torch.float64).numpy()           # exact values of the bf16 weight
+    fwd = oracle.logprob_fwd(Hh, W64, sub.cu_seqlens, sub.mask, sub.targets)
+    # old = logp - ln r*, r* guard-banded 1e-2 away from 1 +- eps:
+    # ~18% of the tokens lie beyond a clip bound, none near one.
+    old = guarded_old_logp(fwd["logp"], np.random.default_rng(17))
+    adv, err = oracle.grpo_advantage(sub.rewards, sub.group_of_seq, sub.num_groups)
+    assert err == 0
+    ref = oracle.policy_loss_fwd_bwd(Hh, W64, sub.cu_seqlens, sub.mask, sub.targets, old, adv,
+                                     n_global=sub.num_tokens)
+    del W64
+    _ORACLE_CACHE[name] = (cfg, sub, H, W, old, adv, ref)
+    return _ORACLE_CACHE[name]
+
+
+@pytest.mark.parametrize("name,mb_rows", [("qwen1.5b", MB_ROWS), ("qwen1.5b", 3000),
+                                          ("openvla", MB_ROWS), ("qwen7b", MB_ROWS),
+                                          ("qwen32b", MB_ROWS)],
+                         ids=["qwen1.5b", "qwen1.5b-multi-mb", "openvla", "qwen7b", "qwen32b"])
+def test_fullsize_oracle_subbatch(rl, name, mb_rows):
+    import torch
+    from paper_2509_15965_b200.dp import PolicyLossStep, device_batch
+    cfg, sub, H, W, old, adv_ref, ref = _oracle_case(name)
+    if not (name == "qwen1.5b" and mb_rows == MB_ROWS):   # reused by the multi-mb case only
+        _ORACLE_CACHE.pop(name)
+    dev = H.device
+    db = device_batch(sub, mb_rows, device=dev)
+    if mb_rows < MB_ROWS:
+        assert len(db.mbs) >= 3          # dW accumulated over several calls
+    head = rl.Head(cfg.hidden, cfg.vocab, cfg.dtype)
+    step = PolicyLossStep(head, W, db, want_entropy=True)
+    gh = torch.full_like(H, 7.0)
+    old_t = torch.as_tensor(old, dtype=torch.float32, device=dev)
+    step.run(H, old_t, gh)
+    torch.cuda.synchronize()
+    R = sub.num_rows
+    act = sub.mask.astype(bool)
+    # advantages (H2) and N (H1)
+    np.testing.assert_allclose(step.adv[:sub.num_seqs].cpu().double().numpy(), adv_ref,
+                               rtol=1e-5, atol=1e-5)
+    assert int(step.n_global.item()) == sub.num_tokens == ref["stats"]["tokens"]
+    # per-row logp / entropy (H3, H4), every row; masked rows exactly 0
+    lp = step.logp[:R].cpu().double().numpy()
+    ent = step.entropy[:R].cpu().double().numpy()
+    assert np.abs(lp - ref["logp"]).max() <= 2e-3
+    assert np.abs(ent - ref["entropy"]).max() <= 2e-3
+    assert (lp[~act] == 0).all() and (ent[~act] == 0).all()
+    # loss statistics (H5)
+    s = rl.read_stats(step.stats)
+    rs = ref["stats"]
+    assert s["tokens"] == rs["tokens"]
+    assert s["clip_hi_count"] == rs["clip_hi_count"] > 0
+    assert s["clip_lo_count"] == rs["clip_lo_count"] > 0
+    assert s["loss_sum"] == pytest.approx(rs["loss_sum"], rel=1e-2)
+    assert s["ratio_sum"] == pytest.approx(rs["ratio_sum"], rel=1e-2)
+    assert s["entropy_sum"] == pytest.approx(rs["entropy_sum"], rel=1e-2)
+    assert s["ratio_max"] == pytest.approx(rs["ratio_max"], rel=1e-2)
+    # dL/dH (H6, H7): every row; masked rows and A = 0 rows exactly 0
+    dH = gh.to(torch.float64).cpu().numpy()
+    assert rel_fro(dH, ref["dH"]) <= 1e-2 and max_rel(dH, ref["dH"]) <= 1e-2
+    assert (dH[~act] == 0).all()
+    zero_rows = act & np.all(ref["dH"] == 0, axis=1)
+    assert zero_rows.any() and (dH[zero_rows] == 0).all()
+    # dL/dW (H8)
+    fro, mrel = _chunked_cmp(step.grad_w, ref["dW"])
+    assert fro <= 1e-2 and mrel <= 1e-2, (fro, mrel)
 
 
 def _first_micro_batch(cfg, seed=0):
@@ -96,7 +256,7 @@ def test_fullsize_sampled_rows(rl, name):
 
 @pytest.mark.parametrize("name", ["qwen7b"])
 def test_fullsize_dw_linearity(rl, name):
-    """dW of one 65k-row micro-batch == dW of its two halves accumulated by two
+    """dW of one 16k-row micro-batch == dW of its two halves accumulated by two
     calls (the micro-batch streaming contract), to fp32 rounding."""
     import torch
     cfg = CONFIGS[name]
@@ -119,6 +279,7 @@ def test_fullsize_dw_linearity(rl, name):
                                   torch.empty(len(rows), cfg.hidden, dtype=H.dtype, device=dev), gw)
 
     S = mb.num_seqs
+    assert S >= 2
     g1 = torch.zeros(cfg.vocab, cfg.hidden, device=dev)
     run(np.arange(S), g1)
     g2 = torch.zeros_like(g1)

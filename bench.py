@@ -57,6 +57,8 @@ def parse():
     p.add_argument("--collective", default="symm", choices=["symm", "nccl"],
                    help="N>1 dW reduction: reduce-scatter fused into the last dW GEMM epilogue "
                         "+ NVLink all-gather (symm), or NCCL all-reduce")
+    p.add_argument("--phases", action="store_true",
+                   help="per-phase step times (always on for N > 1)")
     p.add_argument("--no-aux", action="store_true",
                    help="skip the auxiliary lines (forward-only path, HBM kernels)")
     return p.parse_args()
@@ -382,6 +384,24 @@ def main():
     value = tokens_global / (ms_per_step / 1e3)
     per_step = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]   # this rank
 
+    # per-phase device time of one extra (untimed) step, max over ranks: the
+    # fixed costs that decide strong scaling (zero dW, N all-reduce, advantage,
+    # micro-batches, dW reduction, stats all-gather)
+    phases = None
+    if world > 1 or args.phases:
+        step.timer.enabled = True
+        step.run(H, old, gh)
+        torch.cuda.synchronize()
+        ph = step.timer.ms()
+        step.timer.enabled = False
+        keys = ["zero_dw", "count_allreduce", "advantage", "micro_batches", "dw_reduce",
+                "stats_gather"]
+        t = torch.tensor([ph.get(k, 0.0) for k in keys], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        phases = {k: round(float(v), 3) for k, v in zip(keys, t.tolist())}
+        phases["note"] = "one extra untimed step, ms per phase, max over ranks"
+
     # roofline of the dominant kernel (GEMM kinds: 2hV flops per token per launch)
     pk = peaks()
     kinds = tr.by_kind()
@@ -444,7 +464,7 @@ def main():
                        "lpt_load_max_over_mean": round(float(loads.max() / loads.mean()), 4),
                        "partial": bool(args.max_mb)},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-            "clocks": clocks, "kernels": per_kind, "aux": aux,
+            "clocks": clocks, "kernels": per_kind, "phases_ms": phases, "aux": aux,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -523,7 +543,61 @@ def run_aux(rl, head, H, W, db, mine, step, kinds, tokens_local, tokens_global, 
         out["merge"] = {"launches": n, "ms_per_launch": round(t / max(n, 1), 4),
                         "gbs": round(g, 1), "frac_hbm": round(g / pk["hbm"], 4),
                         "bytes_per_token": 12 * n_vt + 30}
+    if world == 1 and cfg.dtype == "bf16":
+        out["torch_eager_reference"] = torch_reference(H, W, db, mine, step, cfg)
     return out
+
+
+def torch_reference(H, W, db, mine, step, cfg, n_mb=2, chunk=4096):
+    """A library baseline for context (not the headline, not the oracle): the
+    same micro-batch step written the usual way in PyTorch on the GPU --
+    cuBLAS bf16 logits materialised per row chunk, log-softmax, gather, the
+    clipped surrogate, autograd for dL/dH and dL/dW (bf16 parameter grads) --
+    over the first `n_mb` micro-batches, CUDA-event timed after a warm-up."""
+    import torch
+    dev = H.device
+    Wp = W.detach().clone().requires_grad_(True)
+    old = step.logp.detach().clone() + 0.01       # any fixed old log-probs
+
+    def one(r0, r1, s0, s1):
+        mask = db.mask[r0:r1].bool()
+        rows = torch.nonzero(mask).squeeze(1)
+        if rows.numel() == 0:
+            return 0
+        seq = torch.repeat_interleave(torch.arange(s1 - s0, device=dev),
+                                      (db.mbs_cu_np[s0 + 1:s1 + 1] - db.mbs_cu_np[s0:s1]))[rows]
+        A = step.adv[s0:s1][seq]
+        N = float(db.num_tokens)
+        for c0 in range(0, rows.numel(), chunk):
+            rr = rows[c0:c0 + chunk]
+            h = H[r0:r1][rr].detach().requires_grad_(True)
+            z = (h @ Wp.t()).float()
+            logp = torch.log_softmax(z, dim=-1).gather(1, db.targets[r0:r1][rr].long()[:, None])[:, 0]
+            r = torch.exp(torch.clamp(logp - old[r0:r1][rr], -20, 20))
+            a = A[c0:c0 + chunk]
+            loss = torch.maximum(-a * r, -a * torch.clamp(r, 0.8, 1.2)).sum() / N
+            loss.backward()
+        return rows.numel()
+
+    mbs = db.mbs[:n_mb]
+    db.mbs_cu_np = db.cu.cpu().numpy().astype(np.int64)
+    for (s0, s1, r0, r1, _) in mbs[:1]:
+        one(r0, r1, s0, s1)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    tok = 0
+    for (s0, s1, r0, r1, _) in mbs:
+        tok += one(r0, r1, s0, s1)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    del Wp
+    torch.cuda.empty_cache()
+    return {"value": round(tok / (ms / 1e3), 1), "unit": "tokens/s", "tokens": tok,
+            "ms": round(ms, 3), "micro_batches": len(mbs), "row_chunk": chunk,
+            "what": "PyTorch eager bf16 on this GPU: cuBLAS logits materialised per chunk, "
+                    "log_softmax, clipped surrogate, autograd dH/dW (bf16 grads); context only"}
 
 
 def run_e2e(args, rl, step, db, mine, H, old, gh, dev, world, tokens_global):

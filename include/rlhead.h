@@ -261,6 +261,16 @@ RL_API rl_status rl_policy_loss_fwd_bwd(const rl_head *hd, const void *hidden, c
                                  void *grad_hidden, float *grad_weight, rl_loss_stats *stats,
                                  void *ws, size_t ws_bytes, rl_stream_t stream);
 
+/* rl_loss_stats_reduce: *out := the combination of nranks rl_loss_stats
+ * gathered from the DP ranks (device array gathered[nranks], e.g. one NCCL
+ * all-gather of the 72-B struct): the fp64/int64 fields summed in rank
+ * order (deterministic), ratio_max the maximum. Replaces three all-reduces
+ * (SUM fp64, MAX fp32, SUM int64) by one all-gather.
+ * out may not alias gathered. RL_ERR_INVALID_ARG: null pointer or
+ * nranks < 1 (nothing launched). */
+RL_API rl_status rl_loss_stats_reduce(const rl_loss_stats *gathered, int32_t nranks,
+                                      rl_loss_stats *out, rl_stream_t stream);
+
 /* ---- mini-batch update control (NEXT-2) ---------------------------------
  * rl_minibatch_early_stop: "discard minibatches with too large importance
  * ratio" (DESIGN.md §3 #29). From the (all-reduced) device stats:
@@ -399,7 +409,8 @@ typedef enum {
   RL_K_GEMM_DZ = 4, RL_K_GEMM_DH = 5, RL_K_GEMM_DW = 6, RL_K_GRPO = 7,
   RL_K_SIMT_FWD = 8, RL_K_SIMT_BWD = 9, RL_K_REDUCE = 10, RL_K_MISC = 11,
   RL_K_GEMM_DHDW = 12, /* fused dH + dW launch (two GEMMs of 2hV flop/token each) */
-  RL_K_NUM_KINDS = 13
+  RL_K_DZQ = 13,       /* dZ from the forward's q tiles (HBM pass replacing the recompute) */
+  RL_K_NUM_KINDS = 14
 } rl_kernel_kind;
 
 /* Tracing (not thread-safe; for benchmarks, cf. the worker-group timers of

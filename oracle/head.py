@@ -492,7 +492,10 @@ def merge_shard_partials(parts):
 # accumulated gradient is multiplied by 1/N at the end (the loss is linear).
 # --------------------------------------------------------------------------
 def minibatch_early_stop(stats, max_ratio=0.0, max_mean_ratio=0.0):
-    """True if the mini-batch's update is discarded."""
+    """True if the mini-batch's update is discarded.
+
+    PARITY UNPINNED: the statistic and threshold are a reading (#29); PAPER.md
+    prints nothing that fixes them, so no pin exists outside this rule."""
     if max_ratio > 0 and float(stats["ratio_max"]) > max_ratio:
         return True
     if max_mean_ratio > 0 and stats["tokens"] > 0 and \

@@ -21,7 +21,7 @@ CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(ROOT, "build")
 LIB = os.path.join(PKG, "librlhead.so")
 SOURCES = ["api.cu", "prepare.cu", "grpo.cu", "loss.cu", "simt.cu", "tc_gemm.cu", "update.cu",
-           "ppo.cu", "nvls.cu"]
+           "ppo.cu", "nvls.cu", "dz.cu"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

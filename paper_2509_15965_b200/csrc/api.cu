@@ -45,6 +45,10 @@ static bool force_simt() {
   return e && e[0] == '1';
 }
 static bool use_tc(const rl_head* hd) { return hd->dtype == RL_BF16 && !force_simt(); }
+static bool dz_recompute() {
+  const char* e = std::getenv("RLHEAD_DZ_RECOMPUTE");
+  return e && e[0] == '1';
+}
 
 static size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
 
@@ -55,7 +59,7 @@ bool ws_layout(const rl_head* hd, int64_t R, int want_bwd, WsLayout* L) {
   L->Rp = round_up(R > 0 ? R : 1, 2 * TC_BM);  // whole CTA-pair tiles
   L->n_vt = tc ? ceil_div(V, TC_BN) : 1;
   L->Vp = round_up(V, TC_BN);
-  L->nblk_rows = ceil_div(R, 1024);
+  L->nblk_rows = ceil_div(R, H1_TILE_ROWS);
   L->nblk_loss = ceil_div(L->Rp, 32);  // k_merge: 32 rows per block
   size_t o = 0;
   auto take = [&](size_t bytes) {
@@ -330,6 +334,12 @@ static rl_status loss_impl(const rl_head* hd, const void* hidden, const void* we
   const bool entropy_on = p->entropy_coef > 0.f;
   WsLayout L;
   ws_layout(hd, b->num_rows, 1, &L);
+  // q mode (default on the tensor-core path): the forward also stores the
+  // tile-normalised softmax q, and dZ is built from it by one HBM pass instead
+  // of recomputing the logits (the entropy bonus needs z itself, and the
+  // vocab-parallel call has no forward GEMM: both keep the recompute).
+  // RLHEAD_DZ_RECOMPUTE=1 forces the recompute GEMM.
+  const bool q_mode = use_tc(hd) && !parts_all && !entropy_on && !dz_recompute();
   if (!ws || ws_bytes < L.total) return RL_ERR_WORKSPACE;
   if (!aligned(ws, 256)) return RL_ERR_INVALID_ARG;
   const bool tc = use_tc(hd);
@@ -357,7 +367,7 @@ static rl_status loss_impl(const rl_head* hd, const void* hidden, const void* we
     gathered_parts(a, parts_all, nparts, b->num_rows, L, w);
   } else {
     if (tc) {
-      if ((st = launch_tc_fwd(hd, weight, L, w, s)) != RL_OK) return st;
+      if ((st = launch_tc_fwd(hd, weight, L, w, s, q_mode)) != RL_OK) return st;
     } else {
       if ((st = launch_simt_fwd(hd, hidden, weight, L, w, s)) != RL_OK) return st;
     }
@@ -395,10 +405,11 @@ static rl_status loss_impl(const rl_head* hd, const void* hidden, const void* we
   a.st_i = reinterpret_cast<long long*>(w + L.off_st_i);
   if ((st = launch_merge(L, w, a, s)) != RL_OK) return st;
   if ((st = launch_stats_reduce(L, w, stats, s)) != RL_OK) return st;
+  if (q_mode && (st = launch_dz_from_q(hd, L, w, s)) != RL_OK) return st;
   if (tc)
     return launch_tc_bwd(hd, weight, gh_f32 ? nullptr : grad_hidden,
                          gh_f32 ? static_cast<float*>(grad_hidden) : nullptr, gh_mc,
-                         grad_weight, rs, entropy_on, L, w, s);
+                         grad_weight, rs, entropy_on, L, w, s, q_mode);
   return launch_simt_bwd(hd, hidden, weight, grad_hidden, grad_weight, entropy_on, L, w, s);
 }
 
@@ -424,6 +435,12 @@ rl_status rl_policy_loss_fwd_bwd_vp(const rl_head* hd, const void* hidden, const
   if (nparts < 1 || grad_hidden_fp32 < 0 || grad_hidden_fp32 > 2) return RL_ERR_INVALID_ARG;
   return loss_impl(hd, hidden, weight, b, parts_all, nparts, old_logp, adv, p, logp, entropy,
                    grad_hidden, grad_weight, stats, ws, ws_bytes, stream, grad_hidden_fp32);
+}
+
+rl_status rl_loss_stats_reduce(const rl_loss_stats* gathered, int32_t nranks,
+                               rl_loss_stats* out, rl_stream_t stream) {
+  if (!gathered || !out || nranks < 1) return RL_ERR_INVALID_ARG;
+  return launch_stats_ranks(gathered, nranks, out, reinterpret_cast<cudaStream_t>(stream));
 }
 
 const char* rl_status_string(rl_status s) {

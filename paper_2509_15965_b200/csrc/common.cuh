@@ -32,6 +32,7 @@ struct TraceScope {
 constexpr int TC_BM = 128;   // rows per tcgen05 tile (UMMA M)
 constexpr int TC_BN = 256;   // columns per tile (UMMA N)
 constexpr int TC_BK = 64;    // K per pipeline stage (one 128-B swizzle row)
+constexpr int H1_TILE_ROWS = 1024;  // smallest H1 scan tile (status words per call)
 
 // Vocabulary of the whole (possibly vocab-sharded) head; targets live in it.
 inline int64_t vocab_total(const rl_head* hd) {
@@ -47,7 +48,7 @@ struct WsLayout {
   int64_t R, Rp;          // rows, rows padded to TC_BM (+1 tile of slack)
   int64_t n_vt;           // vocab tiles (partials per row)
   int64_t Vp;             // vocab padded to TC_BN (dZ row stride)
-  int64_t nblk_rows;      // 1024-row blocks of the bookkeeping kernels
+  int64_t nblk_rows;      // H1_TILE_ROWS-row tiles of the bookkeeping scan (status words)
   int64_t nblk_loss;      // 32-row blocks of the merge/loss kernel
   size_t prep_total;      // bytes rl_batch_prepare needs (a prefix of the layout)
   size_t off_hdr, off_flags, off_blkcnt, off_blkoff, off_active, off_rowseq, off_tgt,
@@ -60,7 +61,7 @@ bool ws_layout(const rl_head* hd, int64_t R, int want_bwd, WsLayout* L);
 struct WsHeader {
   int64_t n_active;   // active rows of this call
   int32_t bad_cu;     // malformed cu_seqlens
-  int32_t pad;
+  uint32_t tile_ctr;  // H1 scan: tiles claimed in order (zeroed by k_validate)
   // dynamic tile scheduler of the tensor-core GEMMs, one {claimed, retired}
   // counter pair per GEMM kind; zeroed by k_validate and by the last CTA of
   // every launch that uses it

@@ -1,9 +1,10 @@
 // H2: GRPO group-relative advantage ("normalization must
 // aggregate all responses for a query"; readings DESIGN.md §3
-// #5-#8). One CTA per group; each thread accumulates its strided members in
-// index order, then a fixed-order warp-shuffle + shared-memory reduction
-// (deterministic, fp64). With given (all-reduced) statistics the scan is
-// skipped and only the per-member normalisation runs.
+// #5-#8). k_grpo_seg (below): one pass, segmented by group id with warp
+// match/fold steps, fixed summation order (deterministic, fp64); k_grpo (one
+// CTA per group, each scanning all sequences) only when the groups' shared-
+// memory accumulators would not fit. With given (all-reduced) statistics the
+// scan is skipped and only the per-member normalisation runs.
 #include "kernels.h"
 
 namespace rlh {
@@ -93,14 +94,163 @@ k_grpo(const float* __restrict__ r, const int32_t* __restrict__ gos, int32_t S, 
   }
 }
 
+// Segmented form (default while the per-warp accumulators fit in shared
+// memory, G <= GSEG_MAX_G): ONE pass over the sequences. Warp w owns the
+// contiguous chunk [w S/8, (w+1) S/8) and walks it 32 sequences at a time:
+// a warp-shuffle SEGMENTED inclusive scan over the runs of equal group id
+// (5 shuffle rounds; a GRPO group's responses are adjacent in a packed batch,
+// so a step holds 1-3 runs) leaves each run's (n, sum r, sum r^2, max, -min)
+// in its last lane, which adds it into the warp's shared-memory accumulator
+// of that group; tails of the same group in one step (ids not contiguous)
+// are folded by the lowest such lane in lane order. Thread g then folds the
+// 8 warps' accumulators of group g in warp order and the normalisation pass
+// writes A. O(S + 8 G) work, fixed combination order (deterministic run to
+// run), 12 B of HBM per sequence.
+constexpr int GSEG_WARPS = GRPO_THREADS / 32;
+constexpr int GSEG_MAX_G = 512;
+
+__device__ __forceinline__ GStat gstat_shfl_up(const GStat& v, int d) {
+  return {__shfl_up_sync(0xffffffffu, v.n, d), __shfl_up_sync(0xffffffffu, v.s1, d),
+          __shfl_up_sync(0xffffffffu, v.s2, d), __shfl_up_sync(0xffffffffu, v.mx, d),
+          __shfl_up_sync(0xffffffffu, v.nmn, d)};
+}
+
+__global__ void __launch_bounds__(GRPO_THREADS)
+k_grpo_seg(const float* __restrict__ r, const int32_t* __restrict__ gos, int32_t S, int32_t G,
+           const double* __restrict__ sum_in, const double* __restrict__ max_in, float eps,
+           int32_t unbiased, float* __restrict__ adv, double* __restrict__ sum_out,
+           double* __restrict__ max_out, int32_t* err) {
+  extern __shared__ double gsm[];
+  GStat* acc = reinterpret_cast<GStat*>(gsm);                          // [GSEG_WARPS][G]
+  GStat* stg = acc + static_cast<int64_t>(GSEG_WARPS) * G;             // [GSEG_WARPS][32]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int bad = 0;
+  if (!sum_in) {
+    for (int k = threadIdx.x; k < GSEG_WARPS * G; k += GRPO_THREADS)
+      acc[k] = GStat{0.0, 0.0, 0.0, -INFINITY, -INFINITY};
+    __syncthreads();
+    const int per = ((S + GSEG_WARPS - 1) / GSEG_WARPS + 31) & ~31;
+    const int i0 = w * per, i1 = min(S, i0 + per);
+    GStat* my = acc + static_cast<int64_t>(w) * G;
+    GStat* st = stg + w * 32;
+    constexpr int U = 8;                 // steps whose loads are issued together
+    for (int b0 = i0; b0 < i1; b0 += 32 * U) {
+      int32_t gk[U];
+      float rk[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const int i = b0 + 32 * k + lane;
+        gk[k] = i < i1 ? gos[i] : -1;
+        rk[k] = i < i1 ? r[i] : 0.f;
+      }
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      if (b0 + 32 * k >= i1) break;      // warp-uniform
+      const int i = b0 + 32 * k + lane;
+      int key = -1 - lane;               // invalid / past the end: a run of its own
+      GStat v{0.0, 0.0, 0.0, -INFINITY, -INFINITY};
+      if (i < i1) {
+        const int32_t g = gk[k];
+        if (g >= 0 && g < G) {
+          key = g;
+          const double x = static_cast<double>(rk[k]);
+          v = GStat{1.0, x, x * x, x, -x};
+        } else {
+          bad = 1;
+        }
+      }
+      const int kprev = __shfl_up_sync(0xffffffffu, key, 1);
+      const int knext = __shfl_down_sync(0xffffffffu, key, 1);
+      int f = (lane == 0 || kprev != key) ? 1 : 0;      // run head
+      const bool tail = lane == 31 || knext != key;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {                // segmented inclusive scan
+        const GStat pv = gstat_shfl_up(v, d);
+        const int pf = __shfl_up_sync(0xffffffffu, f, d);
+        if (lane >= d) {
+          if (!f) v = gstat_combine(pv, v);
+          f |= pf;
+        }
+      }
+      st[lane] = v;
+      const int tkey = (tail && key >= 0) ? key : -1 - lane;
+      const uint32_t peers = __match_any_sync(0xffffffffu, tkey);
+      __syncwarp();
+      if (tkey >= 0 && lane == __ffs(peers) - 1) {
+        GStat t = my[key];
+        for (uint32_t m = peers; m; m &= m - 1) t = gstat_combine(t, st[__ffs(m) - 1]);
+        my[key] = t;
+      }
+      __syncwarp();
+    }
+    }
+  } else {
+    for (int i = threadIdx.x; i < S; i += GRPO_THREADS) {
+      const int32_t g = gos[i];
+      if (g < 0 || g >= G) bad = 1;
+    }
+  }
+  bad = __syncthreads_or(bad);
+  if (threadIdx.x == 0 && bad && err) atomicOr(err, RL_DEVERR_GROUP);
+  // per group: fold the warps in order; keep (mu, sigma + eps, degenerate) in slot g
+  for (int g = threadIdx.x; g < G; g += GRPO_THREADS) {
+    GStat t;
+    if (sum_in) {
+      t = {sum_in[3 * g], sum_in[3 * g + 1], sum_in[3 * g + 2], max_in[2 * g], max_in[2 * g + 1]};
+    } else {
+      t = acc[g];
+      for (int k = 1; k < GSEG_WARPS; ++k) t = gstat_combine(t, acc[static_cast<int64_t>(k) * G + g]);
+    }
+    if (sum_out) {
+      sum_out[3 * g] = t.n;
+      sum_out[3 * g + 1] = t.s1;
+      sum_out[3 * g + 2] = t.s2;
+      max_out[2 * g] = t.mx;
+      max_out[2 * g + 1] = t.nmn;
+    }
+    // A = 0 exactly for singleton / zero-variance groups (reading #8).
+    const bool degenerate = (t.n <= 1.0) || (t.mx == -t.nmn);
+    const double mu = t.n > 0 ? t.s1 / t.n : 0.0;
+    double var = t.s2 - t.n * mu * mu;
+    var = var > 0.0 ? var : 0.0;
+    var /= unbiased ? (t.n - 1.0) : t.n;
+    acc[g] = GStat{mu, sqrt(var) + static_cast<double>(eps), degenerate ? 1.0 : 0.0, 0.0, 0.0};
+  }
+  if (!adv) return;
+  __syncthreads();
+  for (int i = threadIdx.x; i < S; i += GRPO_THREADS) {
+    const int32_t g = gos[i];
+    float a = 0.f;
+    if (g >= 0 && g < G) {
+      const GStat t = acc[g];
+      if (t.s2 == 0.0) a = static_cast<float>((static_cast<double>(r[i]) - t.n) / t.s1);
+    }
+    adv[i] = a;
+  }
+}
+
+static size_t grpo_seg_smem(int32_t G) {
+  return (static_cast<size_t>(GSEG_WARPS) * G + GSEG_WARPS * 32) * sizeof(GStat);
+}
+
 rl_status launch_grpo(const float* rewards, const int32_t* gos, int32_t S, int32_t G,
                       const double* sum_in, const double* max_in, float eps, int32_t unbiased,
                       float* adv, double* sum_out, double* max_out, int32_t* err,
                       cudaStream_t s) {
   if (G <= 0 && S <= 0) return RL_OK;
   TraceScope ts(RL_K_GRPO, s);
-  k_grpo<<<G + 1, GRPO_THREADS, 0, s>>>(rewards, gos, S, G, sum_in, max_in, eps, unbiased, adv,
-                                       sum_out, max_out, err);
+  if (G >= 1 && G <= GSEG_MAX_G) {
+    static const cudaError_t attr = cudaFuncSetAttribute(
+        k_grpo_seg, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        static_cast<int>(grpo_seg_smem(GSEG_MAX_G)));
+    if (attr != cudaSuccess) return RL_ERR_CUDA;
+    k_grpo_seg<<<1, GRPO_THREADS, grpo_seg_smem(G), s>>>(rewards, gos, S, G, sum_in, max_in, eps,
+                                                         unbiased, adv, sum_out, max_out, err);
+  } else {
+    // many groups: one CTA per group (each scans all S; G x S work)
+    k_grpo<<<G + 1, GRPO_THREADS, 0, s>>>(rewards, gos, S, G, sum_in, max_in, eps, unbiased, adv,
+                                         sum_out, max_out, err);
+  }
   RLH_CHECK_LAUNCH();
   return RL_OK;
 }

@@ -68,6 +68,8 @@ rl_status launch_merge(const WsLayout& L, char* ws, const MergeArgs& a, cudaStre
 rl_status launch_zy_combine(const float* parts_all, int64_t nparts, int64_t ldr,
                             const WsLayout& L, char* ws, cudaStream_t s);
 rl_status launch_stats_reduce(const WsLayout& L, char* ws, rl_loss_stats* stats, cudaStream_t s);
+rl_status launch_stats_ranks(const rl_loss_stats* gathered, int32_t n, rl_loss_stats* out,
+                             cudaStream_t s);
 
 // CUDA-core path (fp32 exact; also bf16 for cross-checks).
 rl_status launch_simt_fwd(const rl_head* hd, const void* hidden, const void* weight,
@@ -77,15 +79,20 @@ rl_status launch_simt_bwd(const rl_head* hd, const void* hidden, const void* wei
                           const WsLayout& L, char* ws, cudaStream_t s);
 
 // Tensor-core path (bf16, tcgen05/TMEM/TMA).
+// q_out: the epilogue also stores q = e^{z - m_tile} (bf16, 0 at the target)
+// into the dZ buffer for launch_dz_from_q.
 rl_status launch_tc_fwd(const rl_head* hd, const void* weight, const WsLayout& L, char* ws,
-                        cudaStream_t s);
+                        cudaStream_t s, bool q_out = false);
+// dZ = tau^-1 g (onehot - p) in place over the q tiles of launch_tc_fwd(q_out):
+// p = q e^{m_tile - lse} off the target, 1 - p_y = -expm1(z_y - lse) at it.
+rl_status launch_dz_from_q(const rl_head* hd, const WsLayout& L, char* ws, cudaStream_t s);
 // grad_hidden_f32 != NULL: dL/dH as fp32 rows [R, hidden] there instead of
 // bf16 rows into grad_hidden; gh_multicast: grad_hidden_f32 is an NVLS
 // multicast address and the rows are added into every rank's copy.
 rl_status launch_tc_bwd(const rl_head* hd, const void* weight, void* grad_hidden,
                         float* grad_hidden_f32, bool gh_multicast, float* grad_weight,
                         const rl_peer_group* dw_rs, bool entropy_on, const WsLayout& L, char* ws,
-                        cudaStream_t s);
+                        cudaStream_t s, bool dz_ready = false);
 
 int num_sms();
 

@@ -4,13 +4,22 @@
 // Semantics: include/rlhead.h (rl_batch), DESIGN.md §5.
 #include "kernels.h"
 
+#include <cstdlib>
+
 namespace rlh {
 
 constexpr int PREP_THREADS = 256;
-constexpr int PREP_ROWS = 1024;  // rows per block (4 per thread)
+// rows per thread: 8 (2048-row tiles) for whole mini-batches, 4 (1024-row
+// tiles) for micro-batches, so a 16k-row call still spreads over 16 SMs
+// (RLHEAD_H1_ITEMS = 4 | 8 | 16 overrides, for A/B runs)
+constexpr int PREP_ITEMS_BIG = 8, PREP_ITEMS_SMALL = 4;
+static_assert(PREP_THREADS * PREP_ITEMS_SMALL == H1_TILE_ROWS, "workspace status words");
 
-__global__ void k_validate(const int32_t* __restrict__ cu, int32_t S, int64_t R,
-                           WsHeader* hdr, int32_t* err) {
+// Launch 1 of 2: validate cu_seqlens, reset the header (active count, tile
+// claim counter, GEMM tile schedulers) and the scan's tile status words.
+__global__ void __launch_bounds__(1024)
+k_validate(const int32_t* __restrict__ cu, int32_t S, int64_t R, WsHeader* hdr,
+           unsigned long long* __restrict__ status, int64_t ntiles, int32_t* err) {
   int bad = 0;
   for (int64_t i = threadIdx.x; i <= S; i += blockDim.x) {
     const int32_t c = cu[i];
@@ -19,23 +28,21 @@ __global__ void k_validate(const int32_t* __restrict__ cu, int32_t S, int64_t R,
     if (i < S && cu[i + 1] < c) bad = 1;
     if (c < 0 || static_cast<int64_t>(c) > R) bad = 1;
   }
+  for (int64_t i = threadIdx.x; i < ntiles; i += blockDim.x) status[i] = 0ull;
   bad = __syncthreads_or(bad);
   if (threadIdx.x == 0) {
     hdr->bad_cu = bad;
     hdr->n_active = 0;
-  }
-  if (threadIdx.x < 16) {
-    hdr->sched[threadIdx.x >> 1][threadIdx.x & 1] = 0u;
-  }
-  if (threadIdx.x == 0) {
+    hdr->tile_ctr = 0u;
     if (bad && err) atomicOr(err, RL_DEVERR_CU_SEQLENS);
   }
+  if (threadIdx.x < 16) hdr->sched[threadIdx.x >> 1][threadIdx.x & 1] = 0u;
 }
 
-// First index i in [0, n) with cu[i] > t (cu non-decreasing).
-__device__ __forceinline__ int32_t upper_bound_i32(const int32_t* __restrict__ cu, int32_t n,
-                                                   int64_t t) {
-  int32_t lo = 0, hi = n;
+// First index i in [lo, n) with cu[i] > t (cu non-decreasing).
+__device__ __forceinline__ int32_t upper_bound_i32(const int32_t* __restrict__ cu, int32_t lo,
+                                                   int32_t n, int64_t t) {
+  int32_t hi = n;
   while (lo < hi) {
     const int32_t mid = (lo + hi) >> 1;
     if (static_cast<int64_t>(__ldg(cu + mid)) <= t) lo = mid + 1; else hi = mid;
@@ -43,121 +50,168 @@ __device__ __forceinline__ int32_t upper_bound_i32(const int32_t* __restrict__ c
   return lo;
 }
 
-// Rows per thread: ROWS_PT consecutive rows, so the row -> sequence map needs
-// one binary search of cu_seqlens per thread, then a forward walk.
-constexpr int ROWS_PT = PREP_ROWS / PREP_THREADS;
+// Decoupled look-back status word of a tile: flag in the top 2 bits.
+constexpr unsigned long long ST_AGG = 1ull << 62;   // this tile's count only
+constexpr unsigned long long ST_PFX = 2ull << 62;   // inclusive prefix through this tile
+constexpr unsigned long long ST_VAL = (1ull << 62) - 1;
 
-__global__ void __launch_bounds__(PREP_THREADS)
-k_flags(const int32_t* __restrict__ cu, int32_t S, int64_t R, const int32_t* __restrict__ targets,
-        const uint8_t* __restrict__ mask, int32_t V, const WsHeader* __restrict__ hdr,
-        uint8_t* __restrict__ act, int32_t* __restrict__ row_seq, int32_t* __restrict__ blk_cnt,
-        float* zero0, float* zero1, float* zero2, int32_t* err) {
+__device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Launch 2 of 2 (single pass): per row the active flag (mask set, target in
+// range, batch well formed) and its sequence; a block-wide ballot scan of the
+// flags; the tile's global offset by decoupled look-back over the preceding
+// tiles' status words (tiles claimed in order from a counter, so every
+// predecessor is already running); then the compaction in packed order.
+// Rows are lane-interleaved (row = tile * 4096 + it * 256 + thread): every
+// load/store instruction of a warp touches 32 consecutive rows.
+template <int PREP_ITEMS>
+__global__ void __launch_bounds__(PREP_THREADS, PREP_ITEMS <= 8 ? 4 : 2)
+k_flags_compact(const int32_t* __restrict__ cu, int32_t S, int64_t R,
+                const int32_t* __restrict__ targets, const uint8_t* __restrict__ mask, int32_t V,
+                WsHeader* hdr, unsigned long long* status, int64_t ntiles,
+                uint8_t* __restrict__ act, int32_t* __restrict__ row_seq,
+                int32_t* __restrict__ active_idx, int32_t* __restrict__ tgt_c,
+                int32_t* __restrict__ seq_c, int64_t* n_active_user, int64_t* n_accum,
+                float* zero0, float* zero1, float* zero2, int32_t* err) {
+  __shared__ int32_t s_cnt[PREP_ITEMS][PREP_THREADS / 32];
+  __shared__ long long s_tile_total, s_prefix;
+  __shared__ int32_t s_tile;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_tile = static_cast<int32_t>(atomicAdd(&hdr->tile_ctr, 1u));
+  __syncthreads();
+  const int64_t tile = s_tile;
   const int bad = hdr->bad_cu;
-  int cnt = 0, terr = 0;
-  const int64_t t0 = static_cast<int64_t>(blockIdx.x) * PREP_ROWS + threadIdx.x * ROWS_PT;
-  // last sequence s with cu[s] <= t0 (empty sequences skipped), as the binary
-  // search below each row would give
-  int32_t s = (!bad && t0 < R) ? upper_bound_i32(cu, S + 1, t0) - 1 : -1;
+  constexpr int PREP_TILE = PREP_THREADS * PREP_ITEMS;
+  const int64_t base = tile * PREP_TILE + tid;
+  // all of this thread's loads first (16 + 16 independent loads in flight)
+  uint8_t mk[PREP_ITEMS];
+  int32_t tg[PREP_ITEMS];
 #pragma unroll
-  for (int j = 0; j < ROWS_PT; ++j) {
-    const int64_t t = t0 + j;
-    if (t >= R) break;
-    uint8_t a = 0;
-    if (!bad) {
-      while (s < S && static_cast<int64_t>(__ldg(cu + s + 1)) <= t) ++s;
-      if (mask[t]) {
-        const int32_t y = targets[t];
-        if (y >= 0 && y < V) a = 1; else terr = 1;
+  for (int it = 0; it < PREP_ITEMS; ++it) {
+    const int64_t t = base + static_cast<int64_t>(it) * PREP_THREADS;
+    mk[it] = t < R ? mask[t] : 0;
+    tg[it] = t < R ? targets[t] : 0;
+  }
+  uint32_t abits = 0;  // bit it: row base + it * 256 is active
+  int32_t seq[PREP_ITEMS];
+  int terr = 0;
+  // sequence of the first row by binary search, then a forward walk (rows grow
+  // by 256 per item; long walks fall back to a binary search over the rest)
+  int32_t s = (!bad && base < R) ? upper_bound_i32(cu, 0, S + 1, base) - 1 : 0;
+#pragma unroll
+  for (int it = 0; it < PREP_ITEMS; ++it) {
+    const int64_t t = base + static_cast<int64_t>(it) * PREP_THREADS;
+    seq[it] = -1;
+    if (t < R) {
+      uint8_t a = 0;
+      if (!bad) {
+        int steps = 0;
+        while (s < S && static_cast<int64_t>(__ldg(cu + s + 1)) <= t) {
+          if (++steps > 8) {
+            s = upper_bound_i32(cu, s, S + 1, t) - 1;
+            break;
+          }
+          ++s;
+        }
+        seq[it] = s;
+        if (mk[it]) {
+          const int32_t y = tg[it];
+          if (y >= 0 && y < V) a = 1; else terr = 1;
+        }
       }
-    }
-    act[t] = a;
-    row_seq[t] = bad ? -1 : s;
-    cnt += a;
-    if (!a) {
-      if (zero0) zero0[t] = 0.f;
-      if (zero1) zero1[t] = 0.f;
-      if (zero2) zero2[t] = 0.f;
+      act[t] = a;
+      if (row_seq) row_seq[t] = bad ? -1 : s;
+      if (!a) {
+        if (zero0) zero0[t] = 0.f;
+        if (zero1) zero1[t] = 0.f;
+        if (zero2) zero2[t] = 0.f;
+      }
+      abits |= static_cast<uint32_t>(a) << it;
     }
   }
   if (terr && err) atomicOr(err, RL_DEVERR_TARGET);
-  cnt = warp_sum(cnt);
-  __shared__ int wsum[PREP_THREADS / 32];
-  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = cnt;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int tot = 0;
-    for (int w = 0; w < PREP_THREADS / 32; ++w) tot += wsum[w];
-    blk_cnt[blockIdx.x] = tot;
-  }
-}
-
-// Exclusive scan of the per-block counts (one block), total -> header and
-// the optional user counters.
-__global__ void __launch_bounds__(1024)
-k_scan(const int32_t* __restrict__ blk_cnt, int64_t nblk, int64_t* __restrict__ blk_off,
-       WsHeader* hdr, int64_t* n_active_user, int64_t* n_accum) {
-  __shared__ int64_t part[1024];
-  const int64_t per = (nblk + blockDim.x - 1) / blockDim.x;
-  const int64_t b0 = threadIdx.x * per;
-  const int64_t b1 = b0 + per < nblk ? b0 + per : nblk;
-  int64_t sum = 0;
-  for (int64_t b = b0; b < b1; ++b) sum += blk_cnt[b];
-  part[threadIdx.x] = sum;
-  __syncthreads();
-  // Hillis-Steele inclusive scan over 1024 partial sums.
-  for (int o = 1; o < 1024; o <<= 1) {
-    int64_t v = threadIdx.x >= o ? part[threadIdx.x - o] : 0;
-    __syncthreads();
-    part[threadIdx.x] += v;
-    __syncthreads();
-  }
-  int64_t run = threadIdx.x ? part[threadIdx.x - 1] : 0;
-  for (int64_t b = b0; b < b1; ++b) {
-    blk_off[b] = run;
-    run += blk_cnt[b];
-  }
-  if (threadIdx.x == blockDim.x - 1) {
-    const int64_t total = part[blockDim.x - 1];
-    hdr->n_active = total;
-    if (n_active_user) *n_active_user = total;
-    if (n_accum) *n_accum += total;
-  }
-}
-
-__global__ void __launch_bounds__(PREP_THREADS)
-k_compact(int64_t R, const uint8_t* __restrict__ act, const int32_t* __restrict__ row_seq,
-          const int32_t* __restrict__ targets, const int64_t* __restrict__ blk_off,
-          int32_t* __restrict__ active_idx, int32_t* __restrict__ tgt_c,
-          int32_t* __restrict__ seq_c) {
-  // Thread = ROWS_PT consecutive rows (packed order = thread order, then row):
-  // exclusive offset = block offset + warps before + lanes before (shuffle scan).
-  __shared__ int wcnt[PREP_THREADS / 32];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t t0 = static_cast<int64_t>(blockIdx.x) * PREP_ROWS + threadIdx.x * ROWS_PT;
-  uint32_t bits = 0;
+  // counts per (it, warp): the packed order of the tile is it-major, then warp, then lane
 #pragma unroll
-  for (int j = 0; j < ROWS_PT; ++j)
-    if (t0 + j < R && act[t0 + j]) bits |= 1u << j;
-  const int c = __popc(bits);
-  int incl = c;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int v = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += v;
+  for (int it = 0; it < PREP_ITEMS; ++it) {
+    const uint32_t b = __ballot_sync(0xffffffffu, (abits >> it) & 1u);
+    if (lane == 0) s_cnt[it][warp] = __popc(b);
   }
-  if (lane == 31) wcnt[warp] = incl;
   __syncthreads();
-  int woff = 0;
-  for (int w = 0; w < warp; ++w) woff += wcnt[w];
-  int64_t o = blk_off[blockIdx.x] + woff + (incl - c);
+  if (warp == 0) {
+    // exclusive scan of the ITEMS x 8 (it, warp) counts: lane owns PER consecutive
+    constexpr int PER = PREP_ITEMS * (PREP_THREADS / 32) / 32;
+    int32_t* flat = &s_cnt[0][0];
+    int32_t c4[PER], sum = 0;
 #pragma unroll
-  for (int j = 0; j < ROWS_PT; ++j) {
-    if (bits & (1u << j)) {
-      const int64_t t = t0 + j;
-      active_idx[o] = static_cast<int32_t>(t);
-      tgt_c[o] = targets[t];
-      seq_c[o] = row_seq[t];
-      ++o;
+    for (int k = 0; k < PER; ++k) {
+      c4[k] = flat[lane * PER + k];
+      sum += c4[k];
+    }
+    int incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    int run = incl - sum;
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      flat[lane * PER + k] = run;
+      run += c4[k];
+    }
+    const long long agg = __shfl_sync(0xffffffffu, incl, 31);
+    // decoupled look-back
+    long long excl = 0;
+    if (tile == 0) {
+      if (lane == 0) atomicExch(status, ST_PFX | static_cast<unsigned long long>(agg));
+    } else {
+      if (lane == 0) atomicExch(status + tile, ST_AGG | static_cast<unsigned long long>(agg));
+      int64_t j = tile - 1;
+      while (true) {
+        const int64_t idx = j - lane;
+        unsigned long long v = ST_PFX;  // before tile 0: prefix 0
+        if (idx >= 0) {
+          do {
+            v = ld_volatile_u64(status + idx);
+          } while ((v >> 62) == 0ull);
+        }
+        const uint32_t pm = __ballot_sync(0xffffffffu, (v >> 62) == 2ull);
+        const int stop = pm ? __ffs(pm) - 1 : 31;  // nearest predecessor with a prefix
+        long long x = lane <= stop ? static_cast<long long>(v & ST_VAL) : 0ll;
+        x = warp_sum(x);
+        excl += x;
+        if (pm) break;
+        j -= 32;
+      }
+      if (lane == 0)
+        atomicExch(status + tile, ST_PFX | static_cast<unsigned long long>(excl + agg));
+    }
+    if (lane == 0) {
+      s_prefix = excl;
+      s_tile_total = agg;
+      if (tile == ntiles - 1) {  // every row's flag is counted: the batch total
+        const long long total = excl + agg;
+        hdr->n_active = total;
+        if (n_active_user) *n_active_user = total;
+        if (n_accum) *n_accum += total;
+      }
+    }
+  }
+  __syncthreads();
+  const long long pfx = s_prefix;
+  const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int it = 0; it < PREP_ITEMS; ++it) {
+    const uint32_t b = __ballot_sync(0xffffffffu, (abits >> it) & 1u);
+    if ((abits >> it) & 1u) {
+      const long long o = pfx + s_cnt[it][warp] + __popc(b & lt);
+      active_idx[o] = static_cast<int32_t>(base + static_cast<int64_t>(it) * PREP_THREADS);
+      tgt_c[o] = tg[it];
+      seq_c[o] = seq[it];
     }
   }
 }
@@ -193,38 +247,39 @@ rl_status launch_prepare(const rl_head* hd, const rl_batch* b, const WsLayout& L
                          float* zero2, cudaStream_t s) {
   WsHeader* hdr = reinterpret_cast<WsHeader*>(ws + L.off_hdr);
   uint8_t* act = reinterpret_cast<uint8_t*>(ws + L.off_flags);
-  int32_t* blk_cnt = reinterpret_cast<int32_t*>(ws + L.off_blkcnt);
-  int64_t* blk_off = reinterpret_cast<int64_t*>(ws + L.off_blkoff);
-  int32_t* row_seq = row_seq_user ? row_seq_user : reinterpret_cast<int32_t*>(ws + L.off_rowseq);
+  unsigned long long* status = reinterpret_cast<unsigned long long*>(ws + L.off_blkoff);
   int32_t* active_idx =
       active_idx_user ? active_idx_user : reinterpret_cast<int32_t*>(ws + L.off_active);
   int32_t* tgt_c = reinterpret_cast<int32_t*>(ws + L.off_tgt);
   int32_t* seq_c = reinterpret_cast<int32_t*>(ws + L.off_seq);
   const int64_t R = b->num_rows;
+  static const int items_env = [] {
+    const char* e = std::getenv("RLHEAD_H1_ITEMS");
+    return (e && *e) ? std::atoi(e) : 0;
+  }();
+  const int items = (items_env == 4 || items_env == 8 || items_env == 16)
+                        ? items_env
+                        : (R >= (int64_t(1) << 21) ? PREP_ITEMS_BIG : PREP_ITEMS_SMALL);
+  const int64_t ntiles = ceil_div(R, PREP_THREADS * items);
   {
     TraceScope ts(RL_K_PREPARE, s);
-    k_validate<<<1, 1024, 0, s>>>(b->cu_seqlens, b->num_seqs, R, hdr, b->err_flags);
+    k_validate<<<1, 1024, 0, s>>>(b->cu_seqlens, b->num_seqs, R, hdr, status, ntiles,
+                                  b->err_flags);
   }
   RLH_CHECK_LAUNCH();
-  const int64_t nblk = ceil_div(R, PREP_ROWS);
-  if (nblk > 0) {
+  if (ntiles > 0) {
     TraceScope ts(RL_K_PREPARE, s);
-    k_flags<<<static_cast<unsigned>(nblk), PREP_THREADS, 0, s>>>(
+    auto kern = items == 16 ? k_flags_compact<16>
+                : items == 8  ? k_flags_compact<8>
+                              : k_flags_compact<4>;
+    kern<<<static_cast<unsigned>(ntiles), PREP_THREADS, 0, s>>>(
         b->cu_seqlens, b->num_seqs, R, b->targets, b->mask,
-        static_cast<int32_t>(vocab_total(hd)), hdr, act, row_seq, blk_cnt,
-        zero0, zero1, zero2, b->err_flags);
-  }
-  RLH_CHECK_LAUNCH();
-  {
-    TraceScope ts(RL_K_PREPARE, s);
-    k_scan<<<1, 1024, 0, s>>>(blk_cnt, nblk, blk_off, hdr, n_active_user, n_accum);
-  }
-  RLH_CHECK_LAUNCH();
-  if (nblk > 0) {
-    TraceScope ts(RL_K_PREPARE, s);
-    k_compact<<<static_cast<unsigned>(nblk), PREP_THREADS, 0, s>>>(R, act, row_seq, b->targets,
-                                                                    blk_off, active_idx, tgt_c,
-                                                                    seq_c);
+        static_cast<int32_t>(vocab_total(hd)), hdr, status, ntiles, act, row_seq_user,
+        active_idx, tgt_c, seq_c, n_active_user, n_accum, zero0, zero1, zero2, b->err_flags);
+  } else if (n_active_user || n_accum) {
+    // no rows: the counts are 0 (n_accum unchanged); n_active_user := 0
+    if (n_active_user && cudaMemsetAsync(n_active_user, 0, sizeof(int64_t), s) != cudaSuccess)
+      return RL_ERR_CUDA;
   }
   RLH_CHECK_LAUNCH();
   if (nseq_accum && b->num_seqs > 0) {

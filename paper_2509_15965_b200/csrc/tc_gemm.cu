@@ -71,8 +71,9 @@ struct TcCfg {
 template <int CG, int NB, int EPI>
 constexpr int tc_smem_bytes() {
   return TcCfg<CG, NB>::SMEM_BYTES +
-         (EPI == 3 /*EPI_ACC*/ && NB == 2 ? 1024 + TcCfg<CG, NB>::STG_BYTES
-          : EPI == 1 /*EPI_DZ*/           ? 1024 + 4 * 2 * 2048
+         ((EPI == 3 /*EPI_ACC*/ || EPI == 4 /*EPI_BWD*/) && NB == 2
+              ? 1024 + TcCfg<CG, NB>::STG_BYTES
+          : (EPI == 1 /*EPI_DZ*/ || EPI == 0 /*EPI_LSE: q stores*/) ? 1024 + 4 * 2 * 2048
                                           : 0);
 }
 
@@ -122,6 +123,10 @@ struct TcArgs {
   // staging buffer over NVLink (plain stores; the owner sums the slots in
   // rank order afterwards, so the result is deterministic).
   int32_t dz_tma;      // EPI_DZ: stage bf16 32x32 boxes in smem, TMA-store them (tmA2 = dZ map)
+  int32_t q_tma;       // EPI_LSE: also store q = e^{z - m_tile} (0 at the target) as bf16
+                       // 32x32 boxes by TMA (tmA2 = map of the dZ buffer): the backward then
+                       // needs no logits recompute (k_dz_from_q rescales q into dZ in place)
+  int32_t k_serp2;     // k_serp of EPI_BWD's second problem (dW), waves counted from its start
   int32_t k_serp;      // tiles of odd waves (tile / clusters) walk K backwards: the next wave
                        // starts on the operand rows the previous one read last, still in L2
   int32_t acc_red;     // EPI_ACC: 0 load+add+store, 1 red.global.add (L2), 2 TMA reduce-add
@@ -170,7 +175,7 @@ template <int CG, int NB, int AMN, int BMN, int EPI>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
           const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2,
-          const TcArgs args) {
+          const __grid_constant__ CUtensorMap tmC, const TcArgs args) {
   using C = TcCfg<CG, NB>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -195,12 +200,16 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     if constexpr (EPI == EPI_BWD) {
       tma_prefetch_desc(&tmA2);
       tma_prefetch_desc(&tmB2);
+      if (args.acc_red == 2) tma_prefetch_desc(&tmC);
     }
     if constexpr (EPI == EPI_ACC) {
       if (args.acc_red == 2) tma_prefetch_desc(&tmA2);
     }
     if constexpr (EPI == EPI_DZ) {
       if (args.dz_tma) tma_prefetch_desc(&tmA2);
+    }
+    if constexpr (EPI == EPI_LSE) {
+      if (args.q_tma) tma_prefetch_desc(&tmA2);
     }
     for (int i = 0; i < C::STAGES; ++i) {
       mbar_init(full + i, CG);     // CG producers arrive (remote for the peer)
@@ -287,7 +296,8 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         bool second;
         const Prob& P = locate(tile, second, mb, nb);
         const bool amn = EPI == EPI_BWD ? second : (AMN != 0);
-        const bool krev = args.k_serp && ((tile / ncl) & 1);
+        const bool krev = second ? (args.k_serp2 && (((tile - P0.tiles) / ncl) & 1))
+                                 : (args.k_serp && ((tile / ncl) & 1));
         const CUtensorMap* mA = second ? &tmA2 : &tmA;
         const CUtensorMap* mB = second ? &tmB2 : &tmB;
         const int32_t m0 = static_cast<int32_t>(mb * C::TILE_M + rank * TC_BM);
@@ -443,6 +453,71 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         const int valid = args.vocab - n0;  // columns < valid are real vocab ids
         float m = -INFINITY, s = 0.f, u = 0.f, zyv = 0.f;
         bool has_y = false;
+        if (args.q_tma) {
+          // Two passes over the TMEM tile. Pass 1: the tile maximum m (and the
+          // target logit). Pass 2: e = e^{z - m}, the partial sums s, u, and
+          // q = e (0 at the target column) -> bf16 32x32 smem boxes (64-B
+          // swizzle) -> TMA store into the dZ buffer (evict-first). q is the
+          // softmax up to the per-(row, tile) factor e^{m - lse}: k_dz_from_q
+          // turns it into dZ after the merge, instead of a recompute GEMM.
+#pragma unroll 1
+          for (int c = 0; c < TC_BN / 32; ++c) {
+            uint32_t v[32];
+            tmem_ld_32x32b_x32(taddr + c * 32, v);
+            tmem_ld_wait();
+            const int yc = yrel - c * 32;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const float z = __uint_as_float(v[j]) * args.inv_temp;
+              if (c * 32 + j < valid) m = fmaxf(m, z);
+              if (j == yc) {
+                zyv = z;
+                has_y = true;
+              }
+            }
+          }
+          const uint64_t st_pol = l2_policy_evict_first();
+          const float m2 = m * LOG2E, sc2 = args.inv_temp * LOG2E;
+#pragma unroll 1
+          for (int c = 0; c < TC_BN / 32; ++c) {
+            uint32_t v[32];
+            tmem_ld_32x32b_x32(taddr + c * 32, v);
+            tmem_ld_wait();
+            if (c == TC_BN / 32 - 1) release(acc);
+            uint32_t pk[16];
+#pragma unroll
+            for (int j = 0; j < 32; j += 2) {
+              float e2[2];
+#pragma unroll
+              for (int k = 0; k < 2; ++k) {
+                const int col = c * 32 + j + k;
+                // log2-domain d = (z - m) log2 e, clamped so masked columns give e = 0
+                const float d2 = col < valid
+                                     ? fmaxf(fmaf(__uint_as_float(v[j + k]), sc2, -m2), -288.f)
+                                     : -288.f;
+                const float e = ex2_approx(d2);
+                s += e;
+                u = fmaf(e, d2 * (1.f / LOG2E), u);
+                e2[k] = col == yrel ? 0.f : e;
+              }
+              pk[j / 2] = pack_bf16x2(e2[0], e2[1]);
+            }
+            uint8_t* buf = smem + C::STG_OFF + ew * 4096 + (c & 1) * 2048;
+            if (lane == 0) bulk_wait_group_read<1>();
+            __syncwarp();
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              *reinterpret_cast<uint4*>(buf + lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4)) =
+                  make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&tmA2, buf, n0 + c * 32,
+                           static_cast<int32_t>(mb * C::TILE_M + rank * TC_BM + ew * 32), st_pol);
+              bulk_commit_group();
+            }
+          }
+        } else {
 #pragma unroll 1
         for (int c = 0; c < TC_BN / 32; ++c) {
           uint32_t v[32];
@@ -485,6 +560,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           }
         }
         release(acc);
+        }
         if (row_ok) {
           // row-blocked partials [Rp/32][n_vt][32]: a warp's 32 rows are 128 B
           // per vocab tile here, and k_merge streams one row block's n_vt
@@ -599,7 +675,8 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       } else {  // EPI_ACC (or the dW half of EPI_BWD)
         float4* dst = reinterpret_cast<float4*>(args.acc + row * args.ld_acc + n0);
         const bool empty_k = P.num_k == 0;  // keep_empty tile: no MMA ran
-        const bool tma_red = EPI == EPI_ACC && NB == 2 && args.acc_red == 2 && args.rs_world == 0;
+        const bool tma_red =
+            (EPI == EPI_ACC || EPI == EPI_BWD) && NB == 2 && args.acc_red == 2 && args.rs_world == 0;
 #pragma unroll 1
         for (int c = 0; c < C::TILE_N / 32; ++c) {
           uint32_t v[32];
@@ -610,7 +687,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = 0u;
           }
-          if constexpr (EPI == EPI_ACC && NB == 2) {
+          if constexpr ((EPI == EPI_ACC || EPI == EPI_BWD) && NB == 2) {
             if (tma_red) {
               // this warp's 32 rows x 32 columns -> a 128-B-swizzled smem box
               // (16-B chunk j of row r at chunk j ^ (r & 7): conflict-free),
@@ -627,7 +704,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
               fence_proxy_async_smem();
               __syncwarp();
               if (lane == 0) {
-                tma_reduce_add_2d(&tmA2, buf, n0 + c * 32,
+                tma_reduce_add_2d(EPI == EPI_BWD ? &tmC : &tmA2, buf, n0 + c * 32,
                                   static_cast<int32_t>(mb * C::TILE_M + rank * TC_BM + ew * 32));
                 bulk_commit_group();
               }
@@ -680,11 +757,14 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       }
     }
   }
-  if constexpr (EPI == EPI_ACC && NB == 2) {
+  if constexpr ((EPI == EPI_ACC || EPI == EPI_BWD) && NB == 2) {
     if (warp >= 4 && lane == 0 && args.acc_red == 2) bulk_wait_group_all();
   }
   if constexpr (EPI == EPI_DZ) {
     if (warp >= 4 && lane == 0 && args.dz_tma) bulk_wait_group_all();
+  }
+  if constexpr (EPI == EPI_LSE) {
+    if (warp >= 4 && lane == 0 && args.q_tma) bulk_wait_group_all();
   }
   tc_fence_before();
   __syncwarp();
@@ -796,7 +876,8 @@ int tc_cta_group() {
 template <int CG, int NB, int AMN, int BMN, int EPI>
 static rl_status run_gemm(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& a2,
                           const CUtensorMap& b2, const TcArgs& args, int64_t tiles_bound,
-                          int kind, cudaStream_t s, bool persistent = true) {
+                          int kind, cudaStream_t s, bool persistent = true,
+                          const CUtensorMap* c = nullptr) {
   using C = TcCfg<CG, NB>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
@@ -827,8 +908,8 @@ static rl_status run_gemm(const CUtensorMap& a, const CUtensorMap& b, const CUte
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   TraceScope ts(kind, s);
-  if (cudaLaunchKernelEx(&cfg, k_tc_gemm<CG, NB, AMN, BMN, EPI>, a, b, a2, b2, args) !=
-      cudaSuccess)
+  if (cudaLaunchKernelEx(&cfg, k_tc_gemm<CG, NB, AMN, BMN, EPI>, a, b, a2, b2, c ? *c : a,
+                         args) != cudaSuccess)
     return RL_ERR_CUDA;
   RLH_CHECK_LAUNCH();
   return RL_OK;
@@ -910,7 +991,7 @@ static TcArgs base_args(const rl_head* hd, const WsLayout& L, char* ws) {
 }
 
 rl_status launch_tc_fwd(const rl_head* hd, const void* weight, const WsLayout& L, char* ws,
-                        cudaStream_t s) {
+                        cudaStream_t s, bool q_out) {
   const int h = hd->hidden, V = hd->vocab;
   const int cg = tc_cta_group();
   CUtensorMap ma, mb;
@@ -928,19 +1009,26 @@ rl_status launch_tc_fwd(const rl_head* hd, const void* weight, const WsLayout& L
   t.zy = reinterpret_cast<float*>(ws + L.off_zy);
   kind_policy(t, "RLHEAD_L2_FWD", -1);
   use_sched(t, ws, L, 0);
-  return run_narrow<0, 0, EPI_LSE>(ma, mb, t, L.Rp, RL_K_GEMM_LSE, s);
+  CUtensorMap mq;
+  if (q_out) {  // q tiles into the dZ buffer [Rp, Vp] (bf16, 32x32 TMA store boxes)
+    t.q_tma = 1;
+    if (!make_map_bf16_32(&mq, ws + L.off_dz, V, L.Rp, static_cast<uint64_t>(L.Vp) * 2))
+      return RL_ERR_CUDA;
+  }
+  return run_narrow<0, 0, EPI_LSE>(ma, mb, t, L.Rp, RL_K_GEMM_LSE, s, q_out ? &mq : nullptr);
 }
 
 rl_status launch_tc_bwd(const rl_head* hd, const void* weight, void* grad_hidden,
                         float* grad_hidden_f32, bool gh_multicast, float* grad_weight,
                         const rl_peer_group* dw_rs, bool entropy_on, const WsLayout& L, char* ws,
-                        cudaStream_t s) {
+                        cudaStream_t s, bool dz_ready) {
   const int h = hd->hidden, V = hd->vocab;
   const int cg = tc_cta_group();
   __nv_bfloat16* dz = reinterpret_cast<__nv_bfloat16*>(ws + L.off_dz);
   rl_status st;
-  // N5: recompute logits, dZ = tau^-1 g (onehot - p) -> bf16 [Rp, Vp].
-  {
+  // N5: recompute logits, dZ = tau^-1 g (onehot - p) -> bf16 [Rp, Vp] (unless
+  // k_dz_from_q already built dZ from the forward's q tiles).
+  if (!dz_ready) {
     CUtensorMap ma, mb;
     if (!make_map(&ma, ws + L.off_hc, h, L.Rp, static_cast<uint64_t>(h) * 2, TC_BM) ||
         !make_map(&mb, weight, h, V, static_cast<uint64_t>(h) * 2, TC_BN / cg))
@@ -1030,12 +1118,22 @@ rl_status launch_tc_bwd(const rl_head* hd, const void* weight, void* grad_hidden
     t.acc = grad_weight;
     t.ld_acc = h;
     t.acc_red = t7.acc_red;
+    t.k_serp2 = t7.k_serp;   // dW tiles: serpentine K by dW wave, as in the separate launch
     t.rs_world = t7.rs_world;
     t.rs_rank = t7.rs_rank;
     t.rs_rows = t7.rs_rows;
     for (int q = 0; q < 8; ++q) t.rs_peer[q] = t7.rs_peer[q];
     const int64_t tiles = (ceil_div(L.Rp, 2 * TC_BM) + ceil_div(V, 2 * TC_BM)) * t.n_tiles;
-    return run_gemm<2, 2, 0, 1, EPI_BWD>(ma6, mb6, ma7, mb7, t, tiles, RL_K_GEMM_DHDW, s);
+    // dW accumulation as in the separate launch: TMA reduce-add of 32x32
+    // smem boxes (whole L2 lines) unless the reduce-scatter stores plainly
+    CUtensorMap macc;
+    if (t.acc_red == 2) {
+      if (t.rs_world > 0 || (reinterpret_cast<uintptr_t>(grad_weight) & 15) != 0) t.acc_red = 1;
+      else if (!make_map_f32(&macc, grad_weight, h, V, static_cast<uint64_t>(h) * 4, 32, 32))
+        return RL_ERR_CUDA;
+    }
+    return run_gemm<2, 2, 0, 1, EPI_BWD>(ma6, mb6, ma7, mb7, t, tiles, RL_K_GEMM_DHDW, s, true,
+                                         t.acc_red == 2 ? &macc : nullptr);
   }
   if ((st = run_wide<0, 1, EPI_ROWS>(ma6, mb6, t6, L.Rp, RL_K_GEMM_DH, s)) != RL_OK) return st;
   CUtensorMap macc;

@@ -23,21 +23,29 @@ __global__ void k_early_stop_decide(const rl_loss_stats* __restrict__ st, float 
   *flag = stop;
 }
 
-// x[i] *= s, with s = 0 when *flag (early stop) or s = 1/N when scaling.
+// x[i] *= 1/N when scaling; when *zero_if (early stop) x[i] := 0, stored
+// directly (not multiplied by 0: a discarded update may hold NaN/Inf).
 __global__ void __launch_bounds__(UPD_THREADS)
 k_scale(float* __restrict__ x, int64_t n, const int32_t* __restrict__ zero_if,
         const int64_t* __restrict__ count) {
   float s = 1.f;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * UPD_THREADS;
   if (zero_if) {
     if (*zero_if == 0) return;
-    s = 0.f;
+    float4* x4 = reinterpret_cast<float4*>(x);
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * UPD_THREADS + threadIdx.x; i < n / 4;
+         i += stride)
+      x4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int64_t i = 4 * (n / 4) + static_cast<int64_t>(blockIdx.x) * UPD_THREADS + threadIdx.x;
+         i < n; i += stride)
+      x[i] = 0.f;
+    return;
   } else {
     const long long c = *count;
     s = c > 0 ? static_cast<float>(1.0 / static_cast<double>(c)) : 0.f;
   }
   const int64_t n4 = n / 4;
   float4* x4 = reinterpret_cast<float4*>(x);
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * UPD_THREADS;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * UPD_THREADS + threadIdx.x; i < n4;
        i += stride) {
     float4 v = x4[i];

@@ -124,17 +124,52 @@ def all_reduce_(t, op="sum", group=None):
     return t
 
 
-def reduce_stats_(stats_u8, group=None):
-    """All-reduce a device rl_loss_stats (72 bytes): sums for the fp64/int64
-    fields, max for ratio_max."""
+def reduce_stats_(stats_u8, group=None, combine=None):
+    """C4: ONE all-gather of every rank's 72-B rl_loss_stats, combined on the
+    device in rank order by rl_loss_stats_reduce (fp64/int64 fields summed,
+    ratio_max maxed; deterministic) -- instead of three all-reduces (SUM
+    fp64, MAX fp32, SUM int64). ``combine(gathered, out)`` replaces the
+    combiner (the CPU gloo tests pass a host one; there is no librlhead
+    kernel on a CPU tensor)."""
     import torch
-    d = stats_u8[:40].view(torch.float64)
-    f = stats_u8[40:44].view(torch.float32)
-    i = stats_u8[48:72].view(torch.int64)
-    all_reduce_(d, "sum", group)
-    all_reduce_(f, "max", group)
-    all_reduce_(i, "sum", group)
+    import torch.distributed as dist
+    P = _world(group)
+    if P <= 1:
+        return stats_u8
+    gathered = torch.empty(P * stats_u8.numel(), dtype=torch.uint8, device=stats_u8.device)
+    dist.all_gather_into_tensor(gathered, stats_u8, group=group)
+    if combine is None:
+        from . import rlhead as R
+        combine = R.rl_loss_stats_reduce
+    combine(gathered, stats_u8)
     return stats_u8
+
+
+class PhaseTimer:
+    """Per-phase device time of a step (CUDA events on the current stream):
+    record(name) closes the phase that started at the previous record. Used
+    to break the multi-GPU step into its fixed costs (bench --phases)."""
+
+    def __init__(self, enabled: bool):
+        self.enabled = enabled
+        self.marks = []
+
+    def reset(self):
+        self.marks = []
+
+    def record(self, name):
+        if not self.enabled:
+            return
+        import torch
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        self.marks.append((name, e))
+
+    def ms(self) -> dict:
+        out = {}
+        for (_, a), (name, b) in zip(self.marks[:-1], self.marks[1:]):
+            out[name] = out.get(name, 0.0) + a.elapsed_time(b)
+        return out
 
 
 @dataclass
@@ -183,7 +218,7 @@ class PolicyLossStep:
 
     def __init__(self, head, weight, db: DeviceBatch, params=None, group=None,
                  advantage: str = "grpo", collective: str = "nccl", split_groups: bool = False,
-                 want_entropy: bool = False):
+                 want_entropy: bool = False, phases: bool = False):
         import torch
         from . import rlhead as R
         self.R = R
@@ -197,8 +232,10 @@ class PolicyLossStep:
         self.params = params or R.LossParams()
         self.group = group
         dev = weight.device
-        self.n_global = torch.zeros(1, dtype=torch.int64, device=dev)
-        self.n_seqs = torch.zeros(1, dtype=torch.int64, device=dev)
+        # C1: (N, S) in one int64[2] tensor -> one all-reduce per step
+        self.counts = torch.zeros(2, dtype=torch.int64, device=dev)
+        self.n_global = self.counts[0:1]
+        self.n_seqs = self.counts[1:2]
         self.params.n_tokens_global = self.n_global
         self.params.n_seqs_global = self.n_seqs
         self.adv = torch.empty(max(db.cu.shape[0] - 1, 1), dtype=torch.float32, device=dev)
@@ -215,17 +252,16 @@ class PolicyLossStep:
                         if want_entropy else None)
         self.ws = R.Workspace(dev)
         self.ws_prep = R.Workspace(dev)
+        self.timer = PhaseTimer(phases)
 
     def count_tokens(self):
         """N = masked tokens (and S = non-empty sequences, for seq-mean
         aggregation) of the whole mini-batch over all ranks."""
         R = self.R
-        self.n_global.zero_()
-        self.n_seqs.zero_()
+        self.counts.zero_()
         R.rl_batch_prepare(self.head, R.Batch(self.db.cu, self.db.targets, self.db.mask),
                            n_accum=self.n_global, nseq_accum=self.n_seqs, ws=self.ws_prep)
-        all_reduce_(self.n_global, "sum", self.group)
-        all_reduce_(self.n_seqs, "sum", self.group)
+        all_reduce_(self.counts, "sum", self.group)
 
     def advantages(self):
         """GRPO (groups are rank-local under LPT sharding) or the REINFORCE++
@@ -260,11 +296,16 @@ class PolicyLossStep:
         streaming). grad_hidden is [R, h], or a reused buffer of at least the
         largest micro-batch (its rows then hold the last micro-batch's dH,
         which the trunk backward would consume before the next one)."""
-        R = self.R
+        R, tm = self.R, self.timer
+        tm.reset()
+        tm.record("start")
         self.grad_w.zero_()
-        self.count_tokens()
-        self.advantages()
         self.stats.zero_()
+        tm.record("zero_dw")
+        self.count_tokens()
+        tm.record("count_allreduce")
+        self.advantages()
+        tm.record("advantage")
         full_gh = grad_hidden.shape[0] >= self.db.num_rows
         last = len(self.db.mbs) - 1
         for i, (s0, s1, r0, r1, cu_mb) in enumerate(self.db.mbs):
@@ -280,12 +321,15 @@ class PolicyLossStep:
             if after_mb:
                 after_mb(i)
         self.params.dw_reduce_scatter = None
+        tm.record("micro_batches")
         if self.symm is not None:
             _symm_dw_finish(R, self.symm, self.staging, self.grad_w, self.peer_group,
                             self.out_peers)
         else:
             all_reduce_(self.grad_w, "sum", self.group)
+        tm.record("dw_reduce")
         reduce_stats_(self.stats, self.group)
+        tm.record("stats_gather")
         return self.stats
 
 

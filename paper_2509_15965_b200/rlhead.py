@@ -24,7 +24,7 @@ RL_OK, RL_ERR_INVALID_ARG, RL_ERR_UNSUPPORTED, RL_ERR_WORKSPACE, RL_ERR_CUDA = r
 RL_F32, RL_BF16 = 0, 1
 RL_DEVERR_CU_SEQLENS, RL_DEVERR_TARGET, RL_DEVERR_GROUP = 1, 2, 4
 KERNEL_KINDS = ["prepare", "gather", "gemm_lse", "merge", "gemm_dz", "gemm_dh", "gemm_dw",
-                "grpo", "simt_fwd", "simt_bwd", "reduce", "misc", "gemm_dhdw"]
+                "grpo", "simt_fwd", "simt_bwd", "reduce", "misc", "gemm_dhdw", "dz_from_q"]
 # tensor flops per token of each GEMM kind, in units of 2 h V
 GEMM_FLOP_UNITS = {"gemm_lse": 1, "gemm_dz": 1, "gemm_dh": 1, "gemm_dw": 1, "gemm_dhdw": 2}
 
@@ -119,6 +119,8 @@ lib.rl_value_loss_fwd_bwd.restype = C.c_int
 lib.rl_value_loss_fwd_bwd.argtypes = [C.POINTER(rl_head), _vp, _vp, C.c_float, C.POINTER(rl_batch),
                                       _vp, _vp, C.POINTER(rl_value_params), _vp, _vp, _vp, _vp,
                                       _vp, _vp, _sz, _vp]
+lib.rl_loss_stats_reduce.restype = C.c_int
+lib.rl_loss_stats_reduce.argtypes = [_vp, C.c_int32, _vp, _vp]
 lib.rl_status_string.restype = C.c_char_p
 lib.rl_status_string.argtypes = [C.c_int]
 lib.rl_build_info.restype = C.c_char_p
@@ -137,7 +139,7 @@ EXPORTED = ["rl_workspace_size", "rl_batch_prepare", "rl_logprob_fwd", "rl_grpo_
             "rl_minibatch_early_stop", "rl_scale_by_inverse_count", "rl_gae",
             "rl_value_workspace_size", "rl_value_loss_fwd_bwd", "rl_allreduce_sum_f32",
             "rl_cast_rows_bf16", "rl_batch_norm_advantage", "rl_read_device_error",
-            "rl_reduce_bcast_rows_f32"]
+            "rl_reduce_bcast_rows_f32", "rl_loss_stats_reduce"]
 
 
 class RLHeadError(RuntimeError):
@@ -476,6 +478,14 @@ def rl_value_loss_fwd_bwd(head: Head, hidden, w_v, b_v: float, batch: Batch, ret
                                      _ptr(grad_hidden), _ptr(grad_w), _ptr(grad_b), _ptr(stats),
                                      _ptr(buf), buf.numel(), _stream(stream)),
            "rl_value_loss_fwd_bwd")
+
+
+def rl_loss_stats_reduce(gathered, out, stream=None):
+    """out := rank-order combination of gathered [nranks * STATS_BYTES] (uint8)
+    rl_loss_stats (sums; max of ratio_max)."""
+    n = int(gathered.numel()) // STATS_BYTES
+    _check(lib.rl_loss_stats_reduce(_ptr(gathered), n, _ptr(out), _stream(stream)),
+           "rl_loss_stats_reduce")
 
 
 def rl_launch_count() -> int:

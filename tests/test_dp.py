@@ -66,6 +66,27 @@ def _stats_bytes(d):
     return bytes(s)
 
 
+def _host_combine(gathered, out):
+    """Test-side stand-in for rl_loss_stats_reduce on CPU tensors: rank-order
+    sums of the gathered structs, max of ratio_max."""
+    from paper_2509_15965_b200 import rlhead as R
+    n = R.STATS_BYTES
+    raw = gathered.numpy().tobytes()
+    parts = [R.rl_loss_stats.from_buffer_copy(raw[q * n:(q + 1) * n]) for q in range(len(raw) // n)]
+    t = parts[0]
+    for v in parts[1:]:
+        for k in ("loss_sum", "ratio_sum", "entropy_sum", "kl_sum", "objective", "clip_lo_count",
+                  "clip_hi_count", "tokens"):
+            setattr(t, k, getattr(t, k) + getattr(v, k))
+        t.ratio_max = max(t.ratio_max, v.ratio_max)
+    out.copy_(torch_u8(bytes(t)))
+
+
+def torch_u8(b):
+    import torch
+    return torch.frombuffer(bytearray(b), dtype=torch.uint8).clone()
+
+
 def _worker(rank, world, port, out_dir):
     import torch
     import torch.distributed as dist
@@ -90,7 +111,7 @@ def _worker(rank, world, port, out_dir):
     dW = torch.from_numpy(out["dW"].copy())
     all_reduce_(dW, "sum")
     st = torch.frombuffer(bytearray(_stats_bytes(out["stats"])), dtype=torch.uint8).clone()
-    reduce_stats_(st)
+    reduce_stats_(st, combine=_host_combine)   # one all-gather (C4)
     if rank == 0:
         np.save(os.path.join(out_dir, "dW.npy"), dW.numpy())
         with open(os.path.join(out_dir, "stats.bin"), "wb") as f:

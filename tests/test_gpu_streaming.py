@@ -62,11 +62,16 @@ def test_early_stop_matches_rule(rl, max_ratio, max_mean):
     st = torch.frombuffer(bytearray(raw), dtype=torch.uint8).clone().cuda()
     flag = torch.full((1,), -1, dtype=torch.int32, device="cuda")
     gw = torch.ones(1000, 7, device="cuda")
+    gw[3, 2] = float("nan")                 # a discarded update may hold NaN/Inf
+    gw[999, 6] = float("inf")
     rl.rl_minibatch_early_stop(st, flag, gw, max_ratio, max_mean)
     torch.cuda.synchronize()
     want = oracle.head.minibatch_early_stop(stats, max_ratio, max_mean)
     assert int(flag.item()) == int(want)
-    assert float(gw.abs().max()) == (0.0 if want else 1.0)
+    if want:                                # grad_weight := 0 exactly (header contract)
+        assert bool((gw == 0).all())
+    else:
+        assert torch.isnan(gw[3, 2]) and float(gw[0].abs().max()) == 1.0
 
 
 def test_scale_by_inverse_count(rl):

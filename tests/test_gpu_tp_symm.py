@@ -105,3 +105,25 @@ def test_dp2_streaming_fused_reduce_scatter():
         assert m[k]["rel_dW_vs_nccl"] == m["stream-nccl"]["rel_dW_vs_nccl"], res
         assert m[k]["tokens"] == m["nccl"]["tokens"], res
     assert all(v["ranks_identical_dW"] for v in m.values()), res
+
+
+def test_dp2_step_vs_oracle():
+    """The 2-rank DP step (both dW reductions) against the CPU float64 oracle
+    of the un-sharded mini-batch: two whole Qwen-1.5B-head prompt groups, one
+    per rank (LPT), at the bench's 16k-row micro-batches. Reduced dW, reduced
+    stats and every row's logp / entropy / dL/dH within the north_star's bf16
+    tolerances (scripts/dp_oracle_check.py)."""
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29535",
+           os.path.join(ROOT, "scripts", "dp_oracle_check.py"), "--config", "qwen1.5b"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=1200, cwd=ROOT)
+    lines = [x for x in out.stdout.splitlines() if x.startswith("{")]
+    assert lines, out.stderr[-3000:]
+    res = json.loads(lines[-1])
+    assert min(res["rank_tokens"]) > 0, res          # both ranks carry a group
+    for mode, r in res["modes"].items():
+        assert r["ok"], (mode, r)
+    assert out.returncode == 0, out.stderr[-3000:]

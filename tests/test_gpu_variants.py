@@ -29,12 +29,15 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
                                  {"RLHEAD_DYN_SCHED": "1", "RLHEAD_CTA_GROUP": "1"},
                                  {"RLHEAD_DZ_TMA": "1", "RLHEAD_CTA_GROUP": "1"},
                                  {"RLHEAD_DZ_TMA": "1", "RLHEAD_DW_RED": "2",
-                                  "RLHEAD_DYN_SCHED": "1"}],
+                                  "RLHEAD_DYN_SCHED": "1"},
+                                 {"RLHEAD_DZ_RECOMPUTE": "1"},
+                                 {"RLHEAD_DZ_RECOMPUTE": "1", "RLHEAD_FUSED_BWD": "1"}],
                          ids=["cta1", "cta2-narrow", "cta2-wide-fused", "cta2-unfused-raster",
                               "dw-load-store", "dw-red-fused", "dw-tma-reduce", "l2-hints",
                               "dw-serpentine", "non-persistent",
                               "dyn-sched", "dyn-sched-fused", "dyn-sched-cta1",
-                              "dz-tma-cta1", "tma-all-dyn"])
+                              "dz-tma-cta1", "tma-all-dyn", "dz-recompute",
+                              "dz-recompute-fused"])
 def test_variant_parity(env):
     import torch
     if not torch.cuda.is_available():
@@ -148,3 +151,52 @@ def test_schedule_and_store_paths_bit_identical(rl):
         for name, a, b in zip(("logp", "entropy", "dH", "dW"), res[0], other):
             assert torch.equal(a, b), (env, name)
     assert float(res[0][3].abs().max()) > 0
+
+
+def test_fused_backward_bit_identical(rl):
+    """The fused dH + dW launch (RLHEAD_FUSED_BWD=1: one persistent tile
+    space, dH tiles first, so the dH launch's partial last wave fills with dW
+    tiles) runs every tile exactly as the two separate launches do -- same K
+    order (serpentine dW waves counted from the first dW tile), same TMA
+    reduce-add of the dW boxes -- so dH and dW must be bit-identical, over a
+    problem with several dH and dW waves and a ragged V."""
+    import numpy as np
+    import torch
+    from tests.gpu_util import dev_tensors
+    from workload import custom_layout
+    rng = np.random.default_rng(13)
+    V, h = 40007, 1024
+    lay = custom_layout(rng.integers(0, 40, 40), rng.integers(200, 900, 40), np.arange(40) // 8,
+                        rng.choice([-5.0, 5.0], 40), vocab=V, num_groups=5)
+    d = dev_tensors(lay)
+    g = torch.Generator(device="cuda").manual_seed(7)
+    H = torch.randn(lay.num_rows, h, device="cuda", generator=g).to(torch.bfloat16)
+    W = (torch.randn(V, h, device="cuda", generator=g) * (4 / h ** 0.5)).to(torch.bfloat16)
+    head = rl.Head(h, V, "bf16")
+    old = torch.empty(lay.num_rows, device="cuda")
+    rl.rl_logprob_fwd(head, H, W, rl.Batch(d["cu"], d["targets"], d["mask"], d["err"]), old)
+    adv = torch.linspace(-1, 1, lay.num_seqs, device="cuda")
+    res = {}
+    prev = os.environ.get("RLHEAD_FUSED_BWD")
+    try:
+        for mode in ("0", "1"):
+            os.environ["RLHEAD_FUSED_BWD"] = mode
+            gw = torch.full((V, h), 0.25, device="cuda")
+            gh = torch.empty_like(H)
+            logp = torch.empty(lay.num_rows, device="cuda")
+            tr = rl.Trace(64).start()
+            rl.rl_policy_loss_fwd_bwd(head, H, W, rl.Batch(d["cu"], d["targets"], d["mask"]),
+                                      old, adv, rl.LossParams(), logp, gh, gw)
+            torch.cuda.synchronize()
+            kinds = tr.stop().by_kind()
+            res[mode] = (gh.cpu(), gw.cpu(), kinds)
+    finally:
+        if prev is None:
+            os.environ.pop("RLHEAD_FUSED_BWD", None)
+        else:
+            os.environ["RLHEAD_FUSED_BWD"] = prev
+    assert "gemm_dhdw" in res["1"][2] and "gemm_dh" not in res["1"][2]
+    assert "gemm_dh" in res["0"][2] and "gemm_dw" in res["0"][2]
+    assert torch.equal(res["0"][0], res["1"][0])
+    assert torch.equal(res["0"][1], res["1"][1])
+    assert float((res["0"][1] - 0.25).abs().max()) > 0

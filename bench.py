@@ -411,7 +411,10 @@ def main():
     dom = max(gemm, key=lambda k: gemm[k][1])
     dom_flops = units[dom] * 2.0 * cfg.hidden * cfg.vocab * tokens_local * args.steps
     achieved = dom_flops / (gemm[dom][1] / 1e3) / 1e12
-    step_tflops_exec = 8.0 * cfg.hidden * cfg.vocab * value / 1e12
+    # executed tensor work per token from the GEMM launches actually traced:
+    # 8hV with the dZ recompute GEMM, 6hV (= the algorithmic count) in q mode
+    exec_units = sum(units[k] * gemm[k][0] for k in gemm) / max(gemm["gemm_lse"][0], 1)
+    step_tflops_exec = exec_units * 2.0 * cfg.hidden * cfg.vocab * value / 1e12
     step_tflops_alg = 6.0 * cfg.hidden * cfg.vocab * value / 1e12
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -426,6 +429,7 @@ def main():
             "peak": pk["bf16_sus"], "unit": "TFLOP/s", "frac": round(achieved / pk["bf16_sus"], 4),
             "traffic": traffic, "peak_kind": f"bf16 sustained ({pk['src']})",
             "frac_of_burst": round(achieved / pk["bf16"], 4),
+            "executed_flops_per_token": f"{exec_units:g} x 2hV",
             "step_executed_tflops": round(step_tflops_exec / world, 1),
             "step_executed_frac_burst": round(step_tflops_exec / world / pk["bf16"], 4),
             "step_algorithmic_frac_burst": round(step_tflops_alg / world / pk["bf16"], 4)}
@@ -564,8 +568,8 @@ def torch_reference(H, W, db, mine, step, cfg, n_mb=2, chunk=4096):
         rows = torch.nonzero(mask).squeeze(1)
         if rows.numel() == 0:
             return 0
-        seq = torch.repeat_interleave(torch.arange(s1 - s0, device=dev),
-                                      (db.mbs_cu_np[s0 + 1:s1 + 1] - db.mbs_cu_np[s0:s1]))[rows]
+        lens = torch.as_tensor(db.mbs_cu_np[s0 + 1:s1 + 1] - db.mbs_cu_np[s0:s1], device=dev)
+        seq = torch.repeat_interleave(torch.arange(s1 - s0, device=dev), lens)[rows]
         A = step.adv[s0:s1][seq]
         N = float(db.num_tokens)
         for c0 in range(0, rows.numel(), chunk):

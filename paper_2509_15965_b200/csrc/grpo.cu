@@ -103,11 +103,13 @@ k_grpo(const float* __restrict__ r, const int32_t* __restrict__ gos, int32_t S, 
 // in its last lane, which adds it into the warp's shared-memory accumulator
 // of that group; tails of the same group in one step (ids not contiguous)
 // are folded by the lowest such lane in lane order. Thread g then folds the
-// 8 warps' accumulators of group g in warp order and the normalisation pass
-// writes A. O(S + 8 G) work, fixed combination order (deterministic run to
-// run), 12 B of HBM per sequence.
-constexpr int GSEG_WARPS = GRPO_THREADS / 32;
-constexpr int GSEG_MAX_G = 512;
+// warps' accumulators of group g in warp order and the normalisation pass
+// writes A. 32 warps (a few serial steps each: the kernel is latency-bound)
+// while 32 x G accumulators fit in shared memory (G <= 150), else 8 warps.
+// O(S + warps G) work, fixed combination order (deterministic run to run),
+// 12 B of HBM per sequence.
+constexpr int GSEG_MAX_G = 512;          // 8 warps x 512 groups of accumulators
+constexpr int GSEG_WIDE_MAX_G = 150;     // 32 warps (fewer serial steps) up to this G
 
 __device__ __forceinline__ GStat gstat_shfl_up(const GStat& v, int d) {
   return {__shfl_up_sync(0xffffffffu, v.n, d), __shfl_up_sync(0xffffffffu, v.s1, d),
@@ -115,7 +117,8 @@ __device__ __forceinline__ GStat gstat_shfl_up(const GStat& v, int d) {
           __shfl_up_sync(0xffffffffu, v.nmn, d)};
 }
 
-__global__ void __launch_bounds__(GRPO_THREADS)
+template <int GSEG_WARPS>
+__global__ void __launch_bounds__(GSEG_WARPS * 32)
 k_grpo_seg(const float* __restrict__ r, const int32_t* __restrict__ gos, int32_t S, int32_t G,
            const double* __restrict__ sum_in, const double* __restrict__ max_in, float eps,
            int32_t unbiased, float* __restrict__ adv, double* __restrict__ sum_out,
@@ -126,7 +129,7 @@ k_grpo_seg(const float* __restrict__ r, const int32_t* __restrict__ gos, int32_t
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   int bad = 0;
   if (!sum_in) {
-    for (int k = threadIdx.x; k < GSEG_WARPS * G; k += GRPO_THREADS)
+    for (int k = threadIdx.x; k < GSEG_WARPS * G; k += (GSEG_WARPS * 32))
       acc[k] = GStat{0.0, 0.0, 0.0, -INFINITY, -INFINITY};
     __syncthreads();
     const int per = ((S + GSEG_WARPS - 1) / GSEG_WARPS + 31) & ~31;
@@ -185,7 +188,7 @@ k_grpo_seg(const float* __restrict__ r, const int32_t* __restrict__ gos, int32_t
     }
     }
   } else {
-    for (int i = threadIdx.x; i < S; i += GRPO_THREADS) {
+    for (int i = threadIdx.x; i < S; i += (GSEG_WARPS * 32)) {
       const int32_t g = gos[i];
       if (g < 0 || g >= G) bad = 1;
     }
@@ -193,7 +196,7 @@ k_grpo_seg(const float* __restrict__ r, const int32_t* __restrict__ gos, int32_t
   bad = __syncthreads_or(bad);
   if (threadIdx.x == 0 && bad && err) atomicOr(err, RL_DEVERR_GROUP);
   // per group: fold the warps in order; keep (mu, sigma + eps, degenerate) in slot g
-  for (int g = threadIdx.x; g < G; g += GRPO_THREADS) {
+  for (int g = threadIdx.x; g < G; g += (GSEG_WARPS * 32)) {
     GStat t;
     if (sum_in) {
       t = {sum_in[3 * g], sum_in[3 * g + 1], sum_in[3 * g + 2], max_in[2 * g], max_in[2 * g + 1]};
@@ -218,7 +221,7 @@ k_grpo_seg(const float* __restrict__ r, const int32_t* __restrict__ gos, int32_t
   }
   if (!adv) return;
   __syncthreads();
-  for (int i = threadIdx.x; i < S; i += GRPO_THREADS) {
+  for (int i = threadIdx.x; i < S; i += (GSEG_WARPS * 32)) {
     const int32_t g = gos[i];
     float a = 0.f;
     if (g >= 0 && g < G) {
@@ -229,8 +232,8 @@ k_grpo_seg(const float* __restrict__ r, const int32_t* __restrict__ gos, int32_t
   }
 }
 
-static size_t grpo_seg_smem(int32_t G) {
-  return (static_cast<size_t>(GSEG_WARPS) * G + GSEG_WARPS * 32) * sizeof(GStat);
+static size_t grpo_seg_smem(int32_t G, int warps) {
+  return (static_cast<size_t>(warps) * G + warps * 32) * sizeof(GStat);
 }
 
 rl_status launch_grpo(const float* rewards, const int32_t* gos, int32_t S, int32_t G,
@@ -240,12 +243,20 @@ rl_status launch_grpo(const float* rewards, const int32_t* gos, int32_t S, int32
   if (G <= 0 && S <= 0) return RL_OK;
   TraceScope ts(RL_K_GRPO, s);
   if (G >= 1 && G <= GSEG_MAX_G) {
-    static const cudaError_t attr = cudaFuncSetAttribute(
-        k_grpo_seg, cudaFuncAttributeMaxDynamicSharedMemorySize,
-        static_cast<int>(grpo_seg_smem(GSEG_MAX_G)));
-    if (attr != cudaSuccess) return RL_ERR_CUDA;
-    k_grpo_seg<<<1, GRPO_THREADS, grpo_seg_smem(G), s>>>(rewards, gos, S, G, sum_in, max_in, eps,
-                                                         unbiased, adv, sum_out, max_out, err);
+    static const cudaError_t attr8 = cudaFuncSetAttribute(
+        k_grpo_seg<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        static_cast<int>(grpo_seg_smem(GSEG_MAX_G, 8)));
+    static const cudaError_t attr32 = cudaFuncSetAttribute(
+        k_grpo_seg<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        static_cast<int>(grpo_seg_smem(GSEG_WIDE_MAX_G, 32)));
+    if (attr8 != cudaSuccess || attr32 != cudaSuccess) return RL_ERR_CUDA;
+    if (G <= GSEG_WIDE_MAX_G)
+      k_grpo_seg<32><<<1, 32 * 32, grpo_seg_smem(G, 32), s>>>(rewards, gos, S, G, sum_in, max_in,
+                                                             eps, unbiased, adv, sum_out, max_out,
+                                                             err);
+    else
+      k_grpo_seg<8><<<1, 8 * 32, grpo_seg_smem(G, 8), s>>>(rewards, gos, S, G, sum_in, max_in, eps,
+                                                          unbiased, adv, sum_out, max_out, err);
   } else {
     // many groups: one CTA per group (each scans all S; G x S work)
     k_grpo<<<G + 1, GRPO_THREADS, 0, s>>>(rewards, gos, S, G, sum_in, max_in, eps, unbiased, adv,

@@ -73,9 +73,13 @@ def main():
         # outputs materialised (what an unfused head would do); timed
         # interleaved with ours so both see the same power/clock state.
         Hc = H[torch.as_tensor(np.flatnonzero(mb.mask), device=dev)].contiguous()
+        # real-valued operands (uninitialised memory can be zeros, which draw
+        # less power and clock higher): dZ ~ the magnitude of a softmax gradient
+        gz = torch.Generator(device=dev).manual_seed(9)
+        dZ = (torch.randn(tok, cfg.vocab, generator=gz, device=dev) * 1e-6).to(H.dtype)
         shapes = {"cublas_fwd_HWt": (Hc, W.t()),
-                  "cublas_dH_ZW": (torch.empty(tok, cfg.vocab, dtype=H.dtype, device=dev), W),
-                  "cublas_dW_ZtH": (torch.empty(cfg.vocab, tok, dtype=H.dtype, device=dev), Hc)}
+                  "cublas_dH_ZW": (dZ, W),
+                  "cublas_dW_ZtH": (dZ.t(), Hc)}
     cub = {k: 0.0 for k in shapes}
     tr.start()
     for _ in range(a.reps):

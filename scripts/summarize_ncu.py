@@ -13,7 +13,7 @@ import csv
 import subprocess
 import sys
 
-OURS = ("k_tc_gemm", "k_merge", "k_gather", "k_flags", "k_compact", "k_scan", "k_validate",
+OURS = ("k_tc_gemm", "k_merge", "k_gather", "k_flags", "k_compact", "k_scan", "k_validate", "k_dz",
         "k_grpo", "k_stats_reduce", "k_zero_inactive", "k_simt")
 
 

@@ -57,6 +57,8 @@ def parse():
     p.add_argument("--collective", default="symm", choices=["symm", "nccl"],
                    help="N>1 dW reduction: reduce-scatter fused into the last dW GEMM epilogue "
                         "+ NVLink all-gather (symm), or NCCL all-reduce")
+    p.add_argument("--pipeline", type=int, default=0,
+                   help="1: two-stream micro-batch pipeline (bwd(i) beside fwd(i+1))")
     p.add_argument("--phases", action="store_true",
                    help="per-phase step times (always on for N > 1)")
     p.add_argument("--no-aux", action="store_true",
@@ -334,11 +336,13 @@ def main():
     collective = args.collective if world > 1 else "none"
     try:
         step = PolicyLossStep(head, W, db, group=group,
-                              collective="symm" if collective == "symm" else "nccl")
+                              collective="symm" if collective == "symm" else "nccl",
+                              pipeline=bool(args.pipeline))
     except Exception as e:  # symmetric memory unavailable: NCCL all-reduce instead
         print(f"[bench] collective=symm unavailable ({e}); using nccl", file=sys.stderr)
         collective = "nccl"
-        step = PolicyLossStep(head, W, db, group=group, collective="nccl")
+        step = PolicyLossStep(head, W, db, group=group, collective="nccl",
+                              pipeline=bool(args.pipeline))
     gh = torch.empty(max_mb, cfg.hidden, dtype=H.dtype, device=dev)
     tokens_local = int(sum(int(mine.mask[r0:r1].sum()) for _, _, r0, r1, _ in db.mbs))
     tok_t = torch.tensor([tokens_local], dtype=torch.int64, device=dev)
@@ -462,7 +466,7 @@ def main():
             "config": {"workload": workload_name(cfg),
                        "global_batch_tokens": tokens_global, "micro_batch_rows": args.mb_rows,
                        "micro_batches_per_rank": len(db.mbs), "parallelism": f"dp{world}",
-                       "dw_collective": collective,
+                       "dw_collective": collective, "pipeline": bool(args.pipeline),
                        "l2": "inputs > L2 (hidden rows of the mini-batch ~ "
                              f"{mine.num_rows * cfg.hidden * 2 / 1e9:.1f} GB per rank)",
                        "lpt_load_max_over_mean": round(float(loads.max() / loads.mean()), 4),

@@ -271,6 +271,29 @@ RL_API rl_status rl_policy_loss_fwd_bwd(const rl_head *hd, const void *hidden, c
 RL_API rl_status rl_loss_stats_reduce(const rl_loss_stats *gathered, int32_t nranks,
                                       rl_loss_stats *out, rl_stream_t stream);
 
+/* Split form of rl_policy_loss_fwd_bwd, for pipelining micro-batches (same
+ * arguments for both calls, same ws, stream-ordered fwd before bwd):
+ * rl_policy_loss_fwd runs H1-H5 -- bookkeeping, projection with the online
+ * LSE (and, on the tensor-core path, the tile-normalised softmax q into ws),
+ * loss, dL/dlogp, stats -- writing logp/entropy/stats and leaving the
+ * backward's state in ws; rl_policy_loss_bwd runs H6-H8 from that state --
+ * dZ (from q, or by recomputing the logits), dL/dH, dW += -- writing
+ * grad_hidden and accumulating grad_weight. fwd + bwd on one stream is
+ * bit-identical to rl_policy_loss_fwd_bwd. Between the two calls ws belongs
+ * to this micro-batch; another micro-batch may run in another workspace on
+ * another stream (e.g. bwd(i)'s memory-bound dZ pass beside fwd(i+1)'s GEMM).
+ * Errors as rl_policy_loss_fwd_bwd (both calls validate every argument). */
+RL_API rl_status rl_policy_loss_fwd(const rl_head *hd, const void *hidden, const void *weight,
+                                    const rl_batch *b, const float *old_logp, const float *adv,
+                                    const rl_loss_params *p, float *logp, float *entropy,
+                                    void *grad_hidden, float *grad_weight, rl_loss_stats *stats,
+                                    void *ws, size_t ws_bytes, rl_stream_t stream);
+RL_API rl_status rl_policy_loss_bwd(const rl_head *hd, const void *hidden, const void *weight,
+                                    const rl_batch *b, const float *old_logp, const float *adv,
+                                    const rl_loss_params *p, float *logp, float *entropy,
+                                    void *grad_hidden, float *grad_weight, rl_loss_stats *stats,
+                                    void *ws, size_t ws_bytes, rl_stream_t stream);
+
 /* ---- mini-batch update control (NEXT-2) ---------------------------------
  * rl_minibatch_early_stop: "discard minibatches with too large importance
  * ratio" (DESIGN.md §3 #29). From the (all-reduced) device stats:

@@ -307,7 +307,9 @@ static rl_status loss_impl(const rl_head* hd, const void* hidden, const void* we
                            const float* old_logp, const float* adv, const rl_loss_params* p,
                            float* logp, float* entropy, void* grad_hidden, float* grad_weight,
                            rl_loss_stats* stats, void* ws, size_t ws_bytes, rl_stream_t stream,
-                           int gh_mode = 0) {
+                           int gh_mode = 0, int phase = 3) {
+  // phase bit 1: H1-H5 (forward, loss, dL/dlogp, stats); bit 2: H6-H8 (dZ, dH,
+  // dW) from the state the forward left in ws (same arguments for both).
   const bool gh_f32 = gh_mode != 0, gh_mc = gh_mode == 2;
   if (!head_ok(hd) || !batch_ok(b) || !weight || !p || !logp || !grad_weight)
     return RL_ERR_INVALID_ARG;
@@ -352,14 +354,29 @@ static rl_status loss_impl(const rl_head* hd, const void* hidden, const void* we
   if (tc && (!aligned(hidden, 16) || !aligned(weight, 16) || !aligned(grad_hidden, 16) ||
              !aligned(grad_weight, 16)))
     return RL_ERR_INVALID_ARG;
+  if (phase < 1 || phase > 3) return RL_ERR_INVALID_ARG;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   char* w = static_cast<char*>(ws);
-  rl_status st = launch_prepare(hd, b, L, w, nullptr, nullptr, nullptr, nullptr, nullptr, logp,
-                                entropy, nullptr, s);
-  if (st != RL_OK) return st;
+  rl_status st = RL_OK;
+  // grad_hidden rows of inactive rows := 0 (from H1's active flags). Not in
   // multicast mode: the caller pre-zeroed every copy; plain stores to a
   // multicast address are not allowed, and inactive rows receive no adds.
-  if (!gh_mc && (st = launch_zero_inactive(hd, grad_hidden, L, w, s, gh_f32)) != RL_OK) return st;
+  const bool zero_gh = (phase & 2) && !gh_mc;
+  if (phase == 2) {  // backward only: the forward's state is in ws
+    if (zero_gh && (st = launch_zero_inactive(hd, grad_hidden, L, w, s, gh_f32)) != RL_OK)
+      return st;
+    if (q_mode && (st = launch_dz_from_q(hd, L, w, s)) != RL_OK) return st;
+    if (tc)
+      return launch_tc_bwd(hd, weight, gh_f32 ? nullptr : grad_hidden,
+                           gh_f32 ? static_cast<float*>(grad_hidden) : nullptr, gh_mc,
+                           grad_weight, rs, entropy_on, L, w, s, q_mode);
+    return launch_simt_bwd(hd, hidden, weight, grad_hidden, grad_weight, entropy_on, L, w, s);
+  }
+  st = launch_prepare(hd, b, L, w, nullptr, nullptr, nullptr, nullptr, nullptr, logp, entropy,
+                      nullptr, s);
+  if (st != RL_OK) return st;
+  if (zero_gh && (st = launch_zero_inactive(hd, grad_hidden, L, w, s, gh_f32)) != RL_OK)
+    return st;
   if (tc && (st = launch_gather_bf16(hd, hidden, L, w, s)) != RL_OK) return st;
   MergeArgs a{};
   if (parts_all) {
@@ -405,6 +422,7 @@ static rl_status loss_impl(const rl_head* hd, const void* hidden, const void* we
   a.st_i = reinterpret_cast<long long*>(w + L.off_st_i);
   if ((st = launch_merge(L, w, a, s)) != RL_OK) return st;
   if ((st = launch_stats_reduce(L, w, stats, s)) != RL_OK) return st;
+  if (!(phase & 2)) return RL_OK;
   if (q_mode && (st = launch_dz_from_q(hd, L, w, s)) != RL_OK) return st;
   if (tc)
     return launch_tc_bwd(hd, weight, gh_f32 ? nullptr : grad_hidden,
@@ -422,6 +440,24 @@ rl_status rl_policy_loss_fwd_bwd(const rl_head* hd, const void* hidden, const vo
                                  void* ws, size_t ws_bytes, rl_stream_t stream) {
   return loss_impl(hd, hidden, weight, b, nullptr, 0, old_logp, adv, p, logp, entropy,
                    grad_hidden, grad_weight, stats, ws, ws_bytes, stream);
+}
+
+rl_status rl_policy_loss_fwd(const rl_head* hd, const void* hidden, const void* weight,
+                             const rl_batch* b, const float* old_logp, const float* adv,
+                             const rl_loss_params* p, float* logp, float* entropy,
+                             void* grad_hidden, float* grad_weight, rl_loss_stats* stats,
+                             void* ws, size_t ws_bytes, rl_stream_t stream) {
+  return loss_impl(hd, hidden, weight, b, nullptr, 0, old_logp, adv, p, logp, entropy,
+                   grad_hidden, grad_weight, stats, ws, ws_bytes, stream, 0, 1);
+}
+
+rl_status rl_policy_loss_bwd(const rl_head* hd, const void* hidden, const void* weight,
+                             const rl_batch* b, const float* old_logp, const float* adv,
+                             const rl_loss_params* p, float* logp, float* entropy,
+                             void* grad_hidden, float* grad_weight, rl_loss_stats* stats,
+                             void* ws, size_t ws_bytes, rl_stream_t stream) {
+  return loss_impl(hd, hidden, weight, b, nullptr, 0, old_logp, adv, p, logp, entropy,
+                   grad_hidden, grad_weight, stats, ws, ws_bytes, stream, 0, 2);
 }
 
 rl_status rl_policy_loss_fwd_bwd_vp(const rl_head* hd, const void* hidden, const void* weight,

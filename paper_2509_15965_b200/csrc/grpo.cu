@@ -105,11 +105,11 @@ k_grpo(const float* __restrict__ r, const int32_t* __restrict__ gos, int32_t S, 
 // are folded by the lowest such lane in lane order. Thread g then folds the
 // warps' accumulators of group g in warp order and the normalisation pass
 // writes A. 32 warps (a few serial steps each: the kernel is latency-bound)
-// while 32 x G accumulators fit in shared memory (G <= 150), else 8 warps.
+// while 32 x G accumulators fit in shared memory (G <= 140), else 8 warps.
 // O(S + warps G) work, fixed combination order (deterministic run to run),
 // 12 B of HBM per sequence.
 constexpr int GSEG_MAX_G = 512;          // 8 warps x 512 groups of accumulators
-constexpr int GSEG_WIDE_MAX_G = 150;     // 32 warps (fewer serial steps) up to this G
+constexpr int GSEG_WIDE_MAX_G = 140;     // 32 warps (fewer serial steps) up to this G
 
 __device__ __forceinline__ GStat gstat_shfl_up(const GStat& v, int d) {
   return {__shfl_up_sync(0xffffffffu, v.n, d), __shfl_up_sync(0xffffffffu, v.s1, d),
@@ -249,7 +249,7 @@ rl_status launch_grpo(const float* rewards, const int32_t* gos, int32_t S, int32
     static const cudaError_t attr32 = cudaFuncSetAttribute(
         k_grpo_seg<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
         static_cast<int>(grpo_seg_smem(GSEG_WIDE_MAX_G, 32)));
-    if (attr8 != cudaSuccess || attr32 != cudaSuccess) return RL_ERR_CUDA;
+    if (G <= GSEG_WIDE_MAX_G ? attr32 != cudaSuccess : attr8 != cudaSuccess) return RL_ERR_CUDA;
     if (G <= GSEG_WIDE_MAX_G)
       k_grpo_seg<32><<<1, 32 * 32, grpo_seg_smem(G, 32), s>>>(rewards, gos, S, G, sum_in, max_in,
                                                              eps, unbiased, adv, sum_out, max_out,

@@ -218,7 +218,7 @@ class PolicyLossStep:
 
     def __init__(self, head, weight, db: DeviceBatch, params=None, group=None,
                  advantage: str = "grpo", collective: str = "nccl", split_groups: bool = False,
-                 want_entropy: bool = False, phases: bool = False):
+                 want_entropy: bool = False, phases: bool = False, pipeline: bool = False):
         import torch
         from . import rlhead as R
         self.R = R
@@ -253,6 +253,11 @@ class PolicyLossStep:
         self.ws = R.Workspace(dev)
         self.ws_prep = R.Workspace(dev)
         self.timer = PhaseTimer(phases)
+        # two-stream micro-batch pipeline (split fwd/bwd API, two workspaces)
+        self.pipeline = bool(pipeline) and head.dtype == "bf16"
+        if self.pipeline:
+            self.ws_pipe = [R.Workspace(dev), R.Workspace(dev)]
+            self.aux_stream = torch.cuda.Stream(device=dev)
 
     def count_tokens(self):
         """N = masked tokens (and S = non-empty sequences, for seq-mean
@@ -308,7 +313,9 @@ class PolicyLossStep:
         tm.record("advantage")
         full_gh = grad_hidden.shape[0] >= self.db.num_rows
         last = len(self.db.mbs) - 1
-        for i, (s0, s1, r0, r1, cu_mb) in enumerate(self.db.mbs):
+        if self.pipeline:
+            self._run_pipelined(hidden, old_logp, grad_hidden, full_gh, hidden_for_mb, after_mb)
+        for i, (s0, s1, r0, r1, cu_mb) in enumerate([] if self.pipeline else self.db.mbs):
             hs = hidden_for_mb(i) if hidden_for_mb else hidden[r0:r1]
             gh = grad_hidden[r0:r1] if full_gh else grad_hidden[:r1 - r0]
             b = R.Batch(cu_mb, self.db.targets[r0:r1], self.db.mask[r0:r1], num_rows=r1 - r0)
@@ -331,6 +338,46 @@ class PolicyLossStep:
         reduce_stats_(self.stats, self.group)
         tm.record("stats_gather")
         return self.stats
+
+
+    def _run_pipelined(self, hidden, old_logp, grad_hidden, full_gh, hidden_for_mb, after_mb):
+        """Micro-batches through the split API on two streams and two workspaces:
+        fwd(i) (H1-H5) on the current stream, bwd(i) (H6-H8) on an auxiliary
+        stream once fwd(i) is done, so bwd(i)'s memory-bound dZ pass runs beside
+        fwd(i+1)'s GEMM; fwd(i+2) waits for bwd(i) (its workspace). dW and the
+        stats accumulate in stream order as in the serial loop (same values)."""
+        import torch
+        R = self.R
+        main = torch.cuda.current_stream()
+        aux = self.aux_stream
+        aux.wait_stream(main)                 # dW/stats zeroed, N and A ready
+        last = len(self.db.mbs) - 1
+        ev_b = {}
+        for i, (s0, s1, r0, r1, cu_mb) in enumerate(self.db.mbs):
+            ws = self.ws_pipe[i % 2]
+            if i >= 2:
+                main.wait_event(ev_b.pop(i - 2))
+            hs = hidden_for_mb(i) if hidden_for_mb else hidden[r0:r1]
+            gh = grad_hidden[r0:r1] if full_gh else grad_hidden[:r1 - r0]
+            b = R.Batch(cu_mb, self.db.targets[r0:r1], self.db.mask[r0:r1], num_rows=r1 - r0)
+            args = (self.head, hs, self.W, b, old_logp[r0:r1], self.adv[s0:s1], self.params,
+                    self.logp[r0:r1], gh, self.grad_w)
+            kw = dict(entropy=None if self.entropy is None else self.entropy[r0:r1],
+                      stats=self.stats, ws=ws)
+            self.params.dw_reduce_scatter = None
+            R.rl_policy_loss_fwd(*args, **kw)
+            ev_f = torch.cuda.Event()
+            ev_f.record(main)
+            if after_mb:
+                after_mb(i)                   # hidden rows are in the workspace now
+            with torch.cuda.stream(aux):
+                aux.wait_event(ev_f)
+                self.params.dw_reduce_scatter = (self.peer_group
+                                                 if self.symm is not None and i == last else None)
+                R.rl_policy_loss_bwd(*args, **kw, stream=aux)
+                ev_b[i] = torch.cuda.Event()
+                ev_b[i].record(aux)
+        main.wait_stream(aux)
 
 
 class StreamingPolicyLoss:

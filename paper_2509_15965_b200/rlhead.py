@@ -89,6 +89,9 @@ lib.rl_policy_loss_fwd_bwd.restype = C.c_int
 lib.rl_policy_loss_fwd_bwd.argtypes = [C.POINTER(rl_head), _vp, _vp, C.POINTER(rl_batch), _vp,
                                        _vp, C.POINTER(rl_loss_params), _vp, _vp, _vp, _vp, _vp,
                                        _vp, _sz, _vp]
+for _fn in (lib.rl_policy_loss_fwd, lib.rl_policy_loss_bwd):
+    _fn.restype = C.c_int
+    _fn.argtypes = lib.rl_policy_loss_fwd_bwd.argtypes
 lib.rl_logprob_partials.restype = C.c_int
 lib.rl_logprob_partials.argtypes = [C.POINTER(rl_head), _vp, _vp, C.POINTER(rl_batch), _vp, _vp,
                                     _sz, _vp]
@@ -139,7 +142,8 @@ EXPORTED = ["rl_workspace_size", "rl_batch_prepare", "rl_logprob_fwd", "rl_grpo_
             "rl_minibatch_early_stop", "rl_scale_by_inverse_count", "rl_gae",
             "rl_value_workspace_size", "rl_value_loss_fwd_bwd", "rl_allreduce_sum_f32",
             "rl_cast_rows_bf16", "rl_batch_norm_advantage", "rl_read_device_error",
-            "rl_reduce_bcast_rows_f32", "rl_loss_stats_reduce"]
+            "rl_reduce_bcast_rows_f32", "rl_loss_stats_reduce", "rl_policy_loss_fwd",
+            "rl_policy_loss_bwd"]
 
 
 class RLHeadError(RuntimeError):
@@ -353,6 +357,32 @@ def rl_policy_loss_fwd_bwd(head: Head, hidden, weight, batch: Batch, old_logp, a
                                       _ptr(entropy), _ptr(grad_hidden), _ptr(grad_weight),
                                       _ptr(stats), _ptr(buf), buf.numel(), _stream(stream)),
            "rl_policy_loss_fwd_bwd")
+
+
+def _loss_phase(fn, name, head, hidden, weight, batch, old_logp, adv, params, logp, grad_hidden,
+                grad_weight, entropy=None, stats=None, ws=None, stream=None):
+    hd, b, p = head.c(), batch.c(), params.c()
+    ws = ws or Workspace()
+    buf = ws.get(rl_workspace_size(head, b.num_rows, True))
+    _check(fn(C.byref(hd), _ptr(hidden), _ptr(weight), C.byref(b), _ptr(old_logp), _ptr(adv),
+              C.byref(p), _ptr(logp), _ptr(entropy), _ptr(grad_hidden), _ptr(grad_weight),
+              _ptr(stats), _ptr(buf), buf.numel(), _stream(stream)), name)
+
+
+def rl_policy_loss_fwd(head: Head, hidden, weight, batch: Batch, old_logp, adv,
+                       params: LossParams, logp, grad_hidden, grad_weight, entropy=None,
+                       stats=None, ws: Workspace | None = None, stream=None):
+    """H1-H5 of rl_policy_loss_fwd_bwd (same arguments); the state stays in ws."""
+    _loss_phase(lib.rl_policy_loss_fwd, "rl_policy_loss_fwd", head, hidden, weight, batch,
+                old_logp, adv, params, logp, grad_hidden, grad_weight, entropy, stats, ws, stream)
+
+
+def rl_policy_loss_bwd(head: Head, hidden, weight, batch: Batch, old_logp, adv,
+                       params: LossParams, logp, grad_hidden, grad_weight, entropy=None,
+                       stats=None, ws: Workspace | None = None, stream=None):
+    """H6-H8 of rl_policy_loss_fwd_bwd from the forward's state in ws."""
+    _loss_phase(lib.rl_policy_loss_bwd, "rl_policy_loss_bwd", head, hidden, weight, batch,
+                old_logp, adv, params, logp, grad_hidden, grad_weight, entropy, stats, ws, stream)
 
 
 def rl_logprob_partials(head: Head, hidden, weight, batch: Batch, parts,

@@ -460,48 +460,71 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           // swizzle) -> TMA store into the dZ buffer (evict-first). q is the
           // softmax up to the per-(row, tile) factor e^{m - lse}: k_dz_from_q
           // turns it into dZ after the merge, instead of a recompute GEMM.
+          // Lean inner loops (these warps share issue slots with the MMA
+          // issuer): the max over raw accumulators (tau^-1 > 0), masking only
+          // in the tile that crosses V, the target column patched only in the
+          // one chunk that holds it, u summed in log2 units.
+          const bool full = valid >= TC_BN;  // warp-uniform: no column beyond V
+          float mraw = -INFINITY;
 #pragma unroll 1
           for (int c = 0; c < TC_BN / 32; ++c) {
             uint32_t v[32];
             tmem_ld_32x32b_x32(taddr + c * 32, v);
             tmem_ld_wait();
-            const int yc = yrel - c * 32;
+            if (full) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const float z = __uint_as_float(v[j]) * args.inv_temp;
-              if (c * 32 + j < valid) m = fmaxf(m, z);
-              if (j == yc) {
-                zyv = z;
-                has_y = true;
-              }
+              for (int j = 0; j < 32; ++j) mraw = fmaxf(mraw, __uint_as_float(v[j]));
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (c * 32 + j < valid) mraw = fmaxf(mraw, __uint_as_float(v[j]));
+            }
+            const int yc = yrel - c * 32;
+            if (yc >= 0 && yc < 32) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (j == yc) zyv = __uint_as_float(v[j]) * args.inv_temp;
+              has_y = true;
             }
           }
+          m = mraw * args.inv_temp;
           const uint64_t st_pol = l2_policy_evict_first();
           const float m2 = m * LOG2E, sc2 = args.inv_temp * LOG2E;
+          float u2 = 0.f;                  // sum e (z - m) log2 e
 #pragma unroll 1
           for (int c = 0; c < TC_BN / 32; ++c) {
             uint32_t v[32];
             tmem_ld_32x32b_x32(taddr + c * 32, v);
             tmem_ld_wait();
             if (c == TC_BN / 32 - 1) release(acc);
+            float e[32];
+            if (full) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                const float d2 = fmaf(__uint_as_float(v[j]), sc2, -m2);  // <= 0
+                e[j] = ex2_approx(d2);
+                s += e[j];
+                u2 = fmaf(e[j], d2, u2);
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                const bool ok = c * 32 + j < valid;
+                const float d2 = ok ? fmaf(__uint_as_float(v[j]), sc2, -m2) : 0.f;
+                e[j] = ok ? ex2_approx(d2) : 0.f;
+                s += e[j];
+                u2 = fmaf(e[j], d2, u2);
+              }
+            }
+            const int yc = yrel - c * 32;
+            if (yc >= 0 && yc < 32) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (j == yc) e[j] = 0.f;   // q = 0 at the target: dZ_y comes from z_y
+            }
             uint32_t pk[16];
 #pragma unroll
-            for (int j = 0; j < 32; j += 2) {
-              float e2[2];
-#pragma unroll
-              for (int k = 0; k < 2; ++k) {
-                const int col = c * 32 + j + k;
-                // log2-domain d = (z - m) log2 e, clamped so masked columns give e = 0
-                const float d2 = col < valid
-                                     ? fmaxf(fmaf(__uint_as_float(v[j + k]), sc2, -m2), -288.f)
-                                     : -288.f;
-                const float e = ex2_approx(d2);
-                s += e;
-                u = fmaf(e, d2 * (1.f / LOG2E), u);
-                e2[k] = col == yrel ? 0.f : e;
-              }
-              pk[j / 2] = pack_bf16x2(e2[0], e2[1]);
-            }
+            for (int j = 0; j < 32; j += 2) pk[j / 2] = pack_bf16x2(e[j], e[j + 1]);
             uint8_t* buf = smem + C::STG_OFF + ew * 4096 + (c & 1) * 2048;
             if (lane == 0) bulk_wait_group_read<1>();
             __syncwarp();
@@ -517,6 +540,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
               bulk_commit_group();
             }
           }
+          u = u2 * (1.f / LOG2E);
         } else {
 #pragma unroll 1
         for (int c = 0; c < TC_BN / 32; ++c) {

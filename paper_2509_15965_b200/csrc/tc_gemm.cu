@@ -453,138 +453,95 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         const int valid = args.vocab - n0;  // columns < valid are real vocab ids
         float m = -INFINITY, s = 0.f, u = 0.f, zyv = 0.f;
         bool has_y = false;
-        if (args.q_tma) {
-          // Two passes over the TMEM tile. Pass 1: the tile maximum m (and the
-          // target logit). Pass 2: e = e^{z - m}, the partial sums s, u, and
-          // q = e (0 at the target column) -> bf16 32x32 smem boxes (64-B
-          // swizzle) -> TMA store into the dZ buffer (evict-first). q is the
-          // softmax up to the per-(row, tile) factor e^{m - lse}: k_dz_from_q
-          // turns it into dZ after the merge, instead of a recompute GEMM.
-          // Lean inner loops (these warps share issue slots with the MMA
-          // issuer): the max over raw accumulators (tau^-1 > 0), masking only
-          // in the tile that crosses V, the target column patched only in the
-          // one chunk that holds it, u summed in log2 units.
-          const bool full = valid >= TC_BN;  // warp-uniform: no column beyond V
-          float mraw = -INFINITY;
-#pragma unroll 1
-          for (int c = 0; c < TC_BN / 32; ++c) {
-            uint32_t v[32];
-            tmem_ld_32x32b_x32(taddr + c * 32, v);
-            tmem_ld_wait();
-            if (full) {
-#pragma unroll
-              for (int j = 0; j < 32; ++j) mraw = fmaxf(mraw, __uint_as_float(v[j]));
-            } else {
-#pragma unroll
-              for (int j = 0; j < 32; ++j)
-                if (c * 32 + j < valid) mraw = fmaxf(mraw, __uint_as_float(v[j]));
-            }
-            const int yc = yrel - c * 32;
-            if (yc >= 0 && yc < 32) {
-#pragma unroll
-              for (int j = 0; j < 32; ++j)
-                if (j == yc) zyv = __uint_as_float(v[j]) * args.inv_temp;
-              has_y = true;
-            }
-          }
-          m = mraw * args.inv_temp;
-          const uint64_t st_pol = l2_policy_evict_first();
-          const float m2 = m * LOG2E, sc2 = args.inv_temp * LOG2E;
-          float u2 = 0.f;                  // sum e (z - m) log2 e
-#pragma unroll 1
-          for (int c = 0; c < TC_BN / 32; ++c) {
-            uint32_t v[32];
-            tmem_ld_32x32b_x32(taddr + c * 32, v);
-            tmem_ld_wait();
-            if (c == TC_BN / 32 - 1) release(acc);
-            float e[32];
-            if (full) {
-#pragma unroll
-              for (int j = 0; j < 32; ++j) {
-                const float d2 = fmaf(__uint_as_float(v[j]), sc2, -m2);  // <= 0
-                e[j] = ex2_approx(d2);
-                s += e[j];
-                u2 = fmaf(e[j], d2, u2);
-              }
-            } else {
-#pragma unroll
-              for (int j = 0; j < 32; ++j) {
-                const bool ok = c * 32 + j < valid;
-                const float d2 = ok ? fmaf(__uint_as_float(v[j]), sc2, -m2) : 0.f;
-                e[j] = ok ? ex2_approx(d2) : 0.f;
-                s += e[j];
-                u2 = fmaf(e[j], d2, u2);
-              }
-            }
-            const int yc = yrel - c * 32;
-            if (yc >= 0 && yc < 32) {
-#pragma unroll
-              for (int j = 0; j < 32; ++j)
-                if (j == yc) e[j] = 0.f;   // q = 0 at the target: dZ_y comes from z_y
-            }
-            uint32_t pk[16];
-#pragma unroll
-            for (int j = 0; j < 32; j += 2) pk[j / 2] = pack_bf16x2(e[j], e[j + 1]);
-            uint8_t* buf = smem + C::STG_OFF + ew * 4096 + (c & 1) * 2048;
-            if (lane == 0) bulk_wait_group_read<1>();
-            __syncwarp();
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-              *reinterpret_cast<uint4*>(buf + lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4)) =
-                  make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-            fence_proxy_async_smem();
-            __syncwarp();
-            if (lane == 0) {
-              tma_store_2d(&tmA2, buf, n0 + c * 32,
-                           static_cast<int32_t>(mb * C::TILE_M + rank * TC_BM + ew * 32), st_pol);
-              bulk_commit_group();
-            }
-          }
-          u = u2 * (1.f / LOG2E);
-        } else {
+        // Two passes over the TMEM tile. Pass 1: the tile maximum m (and the
+        // target logit). Pass 2: e = e^{z - m} and the partial sums s, u;
+        // with q_tma also q = e (0 at the target column) -> bf16 32x32 smem
+        // boxes (64-B swizzle) -> TMA store into the dZ buffer (evict-
+        // first). q is the softmax up to the per-(row, tile) factor
+        // e^{m - lse}: k_dz_from_q turns it into dZ after the merge, instead
+        // of a recompute GEMM.
+        // Lean inner loops (these warps share issue slots with the MMA
+        // issuer): the max over raw accumulators (tau^-1 > 0), masking only
+        // in the tile that crosses V, the target column patched only in the
+        // one chunk that holds it, u summed in log2 units.
+        const bool full = valid >= TC_BN;  // warp-uniform: no column beyond V
+        float mraw = -INFINITY;
 #pragma unroll 1
         for (int c = 0; c < TC_BN / 32; ++c) {
           uint32_t v[32];
           tmem_ld_32x32b_x32(taddr + c * 32, v);
           tmem_ld_wait();
-          float z[32];
+          if (full) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            z[j] = __uint_as_float(v[j]) * args.inv_temp;
-            if (c * 32 + j >= valid) z[j] = -INFINITY;
+            for (int j = 0; j < 32; ++j) mraw = fmaxf(mraw, __uint_as_float(v[j]));
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (c * 32 + j < valid) mraw = fmaxf(mraw, __uint_as_float(v[j]));
           }
           const int yc = yrel - c * 32;
           if (yc >= 0 && yc < 32) {
-            has_y = true;
 #pragma unroll
             for (int j = 0; j < 32; ++j)
-              if (j == yc) zyv = z[j];
+              if (j == yc) zyv = __uint_as_float(v[j]) * args.inv_temp;
+            has_y = true;
           }
-          float cm = z[0];
-#pragma unroll
-          for (int j = 1; j < 32; ++j) cm = fmaxf(cm, z[j]);
-          if (cm > m) {
-            if (s > 0.f) {
-              const float f = ex2_approx((m - cm) * LOG2E);
-              u = f * (u + (m - cm) * s);
-              s *= f;
-            }
-            m = cm;
-          }
-          if (m > -INFINITY) {
+        }
+        m = mraw * args.inv_temp;
+        const uint64_t st_pol = l2_policy_evict_first();
+        const float m2 = m * LOG2E, sc2 = args.inv_temp * LOG2E;
+        float u2 = 0.f;                  // sum e (z - m) log2 e
+#pragma unroll 1
+        for (int c = 0; c < TC_BN / 32; ++c) {
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(taddr + c * 32, v);
+          tmem_ld_wait();
+          if (c == TC_BN / 32 - 1) release(acc);
+          float e[32];
+          if (full) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
-              // clamp keeps masked (-inf) columns at e = 0, e*d = 0 (not NaN);
-              // e^{-200} underflows fp32 anyway.
-              const float d = fmaxf(z[j] - m, -200.f);
-              const float e = ex2_approx(d * LOG2E);
-              s += e;
-              u = fmaf(e, d, u);
+              const float d2 = fmaf(__uint_as_float(v[j]), sc2, -m2);  // <= 0
+              e[j] = ex2_approx(d2);
+              s += e[j];
+              u2 = fmaf(e[j], d2, u2);
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const bool ok = c * 32 + j < valid;
+              const float d2 = ok ? fmaf(__uint_as_float(v[j]), sc2, -m2) : 0.f;
+              e[j] = ok ? ex2_approx(d2) : 0.f;
+              s += e[j];
+              u2 = fmaf(e[j], d2, u2);
             }
           }
+          if (!args.q_tma) continue;     // forward only: partials, no q
+          const int yc = yrel - c * 32;
+          if (yc >= 0 && yc < 32) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (j == yc) e[j] = 0.f;   // q = 0 at the target: dZ_y comes from z_y
+          }
+          uint32_t pk[16];
+#pragma unroll
+          for (int j = 0; j < 32; j += 2) pk[j / 2] = pack_bf16x2(e[j], e[j + 1]);
+          uint8_t* buf = smem + C::STG_OFF + ew * 4096 + (c & 1) * 2048;
+          if (lane == 0) bulk_wait_group_read<1>();
+          __syncwarp();
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            *reinterpret_cast<uint4*>(buf + lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4)) =
+                make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmA2, buf, n0 + c * 32,
+                         static_cast<int32_t>(mb * C::TILE_M + rank * TC_BM + ew * 32), st_pol);
+            bulk_commit_group();
+          }
         }
-        release(acc);
-        }
+        u = u2 * (1.f / LOG2E);
         if (row_ok) {
           // row-blocked partials [Rp/32][n_vt][32]: a warp's 32 rows are 128 B
           // per vocab tile here, and k_merge streams one row block's n_vt

@@ -413,11 +413,29 @@ def main():
     units = rl.rlhead.GEMM_FLOP_UNITS        # a fused dH+dW launch does 2 x 2hV per token
     gemm = {k: kinds[k] for k in units if k in kinds}
     dom = max(gemm, key=lambda k: gemm[k][1])
-    dom_flops = units[dom] * 2.0 * cfg.hidden * cfg.vocab * tokens_local * args.steps
+    # rows each GEMM kind runs over: every active row for the forward (and the
+    # recompute); in skip mode the backward GEMMs (dH, dW) only see the rows with
+    # dL/dlogp != 0 -- here all tokens but those of A = 0 groups and the clipped
+    # ones (token-mean loss, no KL in the bench)
+    st_loc = rl.read_stats(step.stats_local)
+    adv_np = step.adv[:mine.num_seqs].cpu().numpy()
+    cu_np = mine.cu_seqlens.astype(np.int64)
+    seq_tok = np.add.reduceat(mine.mask.astype(np.int64), cu_np[:-1]) if mine.num_rows else \
+        np.zeros(0, np.int64)
+    seq_tok = np.where(cu_np[1:] > cu_np[:-1], seq_tok, 0)
+    grad_rows = int(seq_tok[adv_np != 0].sum()) - st_loc["clip_lo_count"] - st_loc["clip_hi_count"]
+    skip = "dz_from_q" in kinds and os.environ.get("RLHEAD_BWD_SKIP", "1") != "0"
+    rows_of = {"gemm_lse": tokens_local, "gemm_dz": tokens_local,
+               "gemm_dh": grad_rows if skip else tokens_local,
+               "gemm_dw": grad_rows if skip else tokens_local,
+               "gemm_dhdw": grad_rows if skip else tokens_local}
+    dom_flops = units[dom] * 2.0 * cfg.hidden * cfg.vocab * rows_of[dom] * args.steps
     achieved = dom_flops / (gemm[dom][1] / 1e3) / 1e12
     # executed tensor work per token from the GEMM launches actually traced:
-    # 8hV with the dZ recompute GEMM, 6hV (= the algorithmic count) in q mode
-    exec_units = sum(units[k] * gemm[k][0] for k in gemm) / max(gemm["gemm_lse"][0], 1)
+    # 8hV with the dZ recompute GEMM, 6hV in q mode, (2 + 4 f) hV in skip mode
+    # (f = share of tokens with a non-zero gradient)
+    exec_units = sum(units[k] * gemm[k][0] * rows_of[k] for k in gemm) / \
+        max(gemm["gemm_lse"][0] * tokens_local, 1)
     step_tflops_exec = exec_units * 2.0 * cfg.hidden * cfg.vocab * value / 1e12
     step_tflops_alg = 6.0 * cfg.hidden * cfg.vocab * value / 1e12
     traffic = None
@@ -426,14 +444,16 @@ def main():
         try:
             tpt = json.load(open(prof)).get(cfg.name, {}).get(dom)
             if tpt:
-                traffic = tpt * tokens_local / max(gemm[dom][0] / args.steps, 1)
+                traffic = tpt * rows_of[dom] / max(gemm[dom][0] / args.steps, 1)
         except Exception:
             traffic = None
     roof = {"bound": "tensor", "kernel": f"k_tc_gemm[{dom}]", "achieved": round(achieved, 1),
             "peak": pk["bf16_sus"], "unit": "TFLOP/s", "frac": round(achieved / pk["bf16_sus"], 4),
             "traffic": traffic, "peak_kind": f"bf16 sustained ({pk['src']})",
             "frac_of_burst": round(achieved / pk["bf16"], 4),
-            "executed_flops_per_token": f"{exec_units:g} x 2hV",
+            "executed_flops_per_token": f"{exec_units:.4g} x 2hV",
+            "backward_rows": {"tokens": tokens_local, "with_gradient": grad_rows,
+                              "skip_zero_gradient_rows": skip},
             "step_executed_tflops": round(step_tflops_exec / world, 1),
             "step_executed_frac_burst": round(step_tflops_exec / world / pk["bf16"], 4),
             "step_algorithmic_frac_burst": round(step_tflops_alg / world / pk["bf16"], 4)}

@@ -45,6 +45,10 @@ static bool force_simt() {
   return e && e[0] == '1';
 }
 static bool use_tc(const rl_head* hd) { return hd->dtype == RL_BF16 && !force_simt(); }
+static bool bwd_skip() {
+  const char* e = std::getenv("RLHEAD_BWD_SKIP");
+  return !(e && e[0] == '0');
+}
 static bool dz_recompute() {
   const char* e = std::getenv("RLHEAD_DZ_RECOMPUTE");
   return e && e[0] == '1';
@@ -91,6 +95,14 @@ bool ws_layout(const rl_head* hd, int64_t R, int want_bwd, WsLayout* L) {
   L->off_st_d = take(static_cast<size_t>(L->nblk_loss) * 5 * 8);
   L->off_st_f = take(static_cast<size_t>(L->nblk_loss) * 4);
   L->off_st_i = take(static_cast<size_t>(L->nblk_loss) * 3 * 8);
+  // backward-row compaction (q mode): rows with dL/dlogp != 0, their dZ and
+  // Hc rows packed densely so dH / dW skip the rows whose gradient is exactly 0
+  const bool bwd_tc = want_bwd && tc;
+  L->off_keep = take(bwd_tc ? static_cast<size_t>(L->Rp) * 4 : 0);
+  L->off_oidx2 = take(bwd_tc ? static_cast<size_t>(L->Rp) * 4 : 0);
+  L->off_st2 = take(bwd_tc ? static_cast<size_t>(ceil_div(L->Rp, H1_TILE_ROWS)) * 8 : 0);
+  L->off_dz2 = take(bwd_tc ? static_cast<size_t>(L->Rp) * L->Vp * 2 : 0);
+  L->off_hc2 = take(bwd_tc ? static_cast<size_t>(L->Rp) * h * 2 : 0);
   L->total = o;
   return true;
 }
@@ -342,6 +354,11 @@ static rl_status loss_impl(const rl_head* hd, const void* hidden, const void* we
   // vocab-parallel call has no forward GEMM: both keep the recompute).
   // RLHEAD_DZ_RECOMPUTE=1 forces the recompute GEMM.
   const bool q_mode = use_tc(hd) && !parts_all && !entropy_on && !dz_recompute();
+  // skip mode (q mode, default): the backward GEMMs run only over the rows with
+  // dL/dlogp != 0 -- GRPO groups whose rewards are all equal (A = 0), clipped
+  // and padding rows have dZ = 0 and contribute exactly nothing to dH / dW.
+  // RLHEAD_BWD_SKIP=0 keeps every active row.
+  const bool skip_rows = q_mode && bwd_skip();
   if (!ws || ws_bytes < L.total) return RL_ERR_WORKSPACE;
   if (!aligned(ws, 256)) return RL_ERR_INVALID_ARG;
   const bool tc = use_tc(hd);
@@ -363,19 +380,21 @@ static rl_status loss_impl(const rl_head* hd, const void* hidden, const void* we
   // multicast address are not allowed, and inactive rows receive no adds.
   const bool zero_gh = (phase & 2) && !gh_mc;
   if (phase == 2) {  // backward only: the forward's state is in ws
-    if (zero_gh && (st = launch_zero_inactive(hd, grad_hidden, L, w, s, gh_f32)) != RL_OK)
+    if (zero_gh &&
+        (st = launch_zero_inactive(hd, grad_hidden, L, w, s, gh_f32, skip_rows)) != RL_OK)
       return st;
-    if (q_mode && (st = launch_dz_from_q(hd, L, w, s)) != RL_OK) return st;
+    if (q_mode && (st = launch_dz_from_q(hd, L, w, s, skip_rows)) != RL_OK) return st;
     if (tc)
       return launch_tc_bwd(hd, weight, gh_f32 ? nullptr : grad_hidden,
                            gh_f32 ? static_cast<float*>(grad_hidden) : nullptr, gh_mc,
-                           grad_weight, rs, entropy_on, L, w, s, q_mode);
+                           grad_weight, rs, entropy_on, L, w, s, q_mode, skip_rows);
     return launch_simt_bwd(hd, hidden, weight, grad_hidden, grad_weight, entropy_on, L, w, s);
   }
   st = launch_prepare(hd, b, L, w, nullptr, nullptr, nullptr, nullptr, nullptr, logp, entropy,
                       nullptr, s);
   if (st != RL_OK) return st;
-  if (zero_gh && (st = launch_zero_inactive(hd, grad_hidden, L, w, s, gh_f32)) != RL_OK)
+  if (zero_gh &&
+      (st = launch_zero_inactive(hd, grad_hidden, L, w, s, gh_f32, skip_rows)) != RL_OK)
     return st;
   if (tc && (st = launch_gather_bf16(hd, hidden, L, w, s)) != RL_OK) return st;
   MergeArgs a{};
@@ -384,7 +403,11 @@ static rl_status loss_impl(const rl_head* hd, const void* hidden, const void* we
     gathered_parts(a, parts_all, nparts, b->num_rows, L, w);
   } else {
     if (tc) {
-      if ((st = launch_tc_fwd(hd, weight, L, w, s, q_mode)) != RL_OK) return st;
+      // with no KL term, A = 0 means dL/dlogp = 0: those rows' q is never read
+      const bool adv_gate = skip_rows && p->kl_coef == 0.f;
+      if ((st = launch_tc_fwd(hd, weight, L, w, s, q_mode, adv_gate ? adv : nullptr,
+                              p->adv_per_token != 0)) != RL_OK)
+        return st;
     } else {
       if ((st = launch_simt_fwd(hd, hidden, weight, L, w, s)) != RL_OK) return st;
     }
@@ -423,11 +446,11 @@ static rl_status loss_impl(const rl_head* hd, const void* hidden, const void* we
   if ((st = launch_merge(L, w, a, s)) != RL_OK) return st;
   if ((st = launch_stats_reduce(L, w, stats, s)) != RL_OK) return st;
   if (!(phase & 2)) return RL_OK;
-  if (q_mode && (st = launch_dz_from_q(hd, L, w, s)) != RL_OK) return st;
+  if (q_mode && (st = launch_dz_from_q(hd, L, w, s, skip_rows)) != RL_OK) return st;
   if (tc)
     return launch_tc_bwd(hd, weight, gh_f32 ? nullptr : grad_hidden,
                          gh_f32 ? static_cast<float*>(grad_hidden) : nullptr, gh_mc,
-                         grad_weight, rs, entropy_on, L, w, s, q_mode);
+                         grad_weight, rs, entropy_on, L, w, s, q_mode, skip_rows);
   return launch_simt_bwd(hd, hidden, weight, grad_hidden, grad_weight, entropy_on, L, w, s);
 }
 

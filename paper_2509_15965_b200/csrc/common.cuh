@@ -53,7 +53,7 @@ struct WsLayout {
   size_t prep_total;      // bytes rl_batch_prepare needs (a prefix of the layout)
   size_t off_hdr, off_flags, off_blkcnt, off_blkoff, off_active, off_rowseq, off_tgt,
       off_seq, off_hc, off_pm, off_ps, off_pu, off_zy, off_lse, off_g, off_ge, off_ez, off_dz,
-      off_st_d, off_st_f, off_st_i, total;
+      off_st_d, off_st_f, off_st_i, off_keep, off_oidx2, off_st2, off_dz2, off_hc2, total;
 };
 bool ws_layout(const rl_head* hd, int64_t R, int want_bwd, WsLayout* L);
 
@@ -66,7 +66,59 @@ struct WsHeader {
   // counter pair per GEMM kind; zeroed by k_validate and by the last CTA of
   // every launch that uses it
   uint32_t sched[8][2];
+  int64_t n_bwd;      // rows with dL/dlogp != 0 (the backward's rows in skip mode)
+  uint32_t tile_ctr2; // backward-row compaction: tiles claimed in order
+  uint32_t pad2;
 };
+
+// ------------------------------------------ decoupled look-back scan ----
+// Status word of a tile of a single-pass scan: flag in the top 2 bits.
+constexpr unsigned long long ST_AGG = 1ull << 62;   // this tile's count only
+constexpr unsigned long long ST_PFX = 2ull << 62;   // inclusive prefix through this tile
+constexpr unsigned long long ST_VAL = (1ull << 62) - 1;
+
+__device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v);
+
+// One warp: publish this tile's count `agg`, look back over the preceding
+// tiles' status words 32 at a time (every predecessor is already running:
+// tiles are claimed in order from a counter) until the nearest one with an
+// inclusive prefix, publish this tile's inclusive prefix; returns the
+// exclusive prefix (all lanes). status[] zeroed before the launch.
+__device__ __forceinline__ long long decoupled_lookback(unsigned long long* status, int64_t tile,
+                                                        long long agg, int lane) {
+  long long excl = 0;
+  if (tile == 0) {
+    if (lane == 0) atomicExch(status, ST_PFX | static_cast<unsigned long long>(agg));
+    return 0;
+  }
+  if (lane == 0) atomicExch(status + tile, ST_AGG | static_cast<unsigned long long>(agg));
+  int64_t j = tile - 1;
+  while (true) {
+    const int64_t idx = j - lane;
+    unsigned long long v = ST_PFX;  // before tile 0: prefix 0
+    if (idx >= 0) {
+      do {
+        v = ld_volatile_u64(status + idx);
+      } while ((v >> 62) == 0ull);
+    }
+    const uint32_t pm = __ballot_sync(0xffffffffu, (v >> 62) == 2ull);
+    const int stop = pm ? __ffs(pm) - 1 : 31;  // nearest predecessor with a prefix
+    long long x = lane <= stop ? static_cast<long long>(v & ST_VAL) : 0ll;
+    x = warp_sum(x);
+    excl += x;
+    if (pm) break;
+    j -= 32;
+  }
+  if (lane == 0) atomicExch(status + tile, ST_PFX | static_cast<unsigned long long>(excl + agg));
+  return excl;
+}
 
 // ------------------------------------------------------ device reductions ----
 template <typename T>

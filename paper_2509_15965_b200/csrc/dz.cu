@@ -20,25 +20,106 @@
 namespace rlh {
 
 constexpr int DZ_THREADS = 256;   // one CTA per row; a warp covers one 256-column vocab tile
+constexpr int KEEP_ITEMS = 4;     // backward-row compaction: 1024-row tiles
 
+// Backward rows (skip mode): the compact rows r < T with dL/dlogp g_r != 0, in
+// order -> keep[r2] = r, oidx2[r2] = active_idx[r] (the packed row dL/dH goes
+// to), hdr->n_bwd = their count. Rows with g = 0 -- every row of a GRPO group
+// whose rewards are all equal (A = 0), clipped rows, padding -- have dZ = 0,
+// so they contribute exactly nothing to dH (written as zeros elsewhere) or dW.
+// Single pass: ballot counts per (item, warp), decoupled look-back across the
+// tiles (claimed in order from a counter).
 __global__ void __launch_bounds__(DZ_THREADS)
-k_dz_from_q(uint4* __restrict__ dz, int64_t ld_vec, int32_t V, int64_t n_vt,
+k_keep_compact(const float* __restrict__ g_c, const int32_t* __restrict__ active_idx,
+               WsHeader* hdr, unsigned long long* status, int64_t ntiles,
+               int32_t* __restrict__ keep, int32_t* __restrict__ oidx2) {
+  __shared__ int32_t s_cnt[KEEP_ITEMS][DZ_THREADS / 32];
+  __shared__ long long s_prefix;
+  __shared__ int32_t s_tile;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_tile = static_cast<int32_t>(atomicAdd(&hdr->tile_ctr2, 1u));
+  __syncthreads();
+  const int64_t tile = s_tile;
+  const int64_t T = hdr->n_active;
+  const int64_t base = tile * (DZ_THREADS * KEEP_ITEMS) + tid;
+  uint32_t kbits = 0;
+#pragma unroll
+  for (int it = 0; it < KEEP_ITEMS; ++it) {
+    const int64_t r = base + static_cast<int64_t>(it) * DZ_THREADS;
+    if (r < T && g_c[r] != 0.f) kbits |= 1u << it;
+  }
+#pragma unroll
+  for (int it = 0; it < KEEP_ITEMS; ++it) {
+    const uint32_t b = __ballot_sync(0xffffffffu, (kbits >> it) & 1u);
+    if (lane == 0) s_cnt[it][warp] = __popc(b);
+  }
+  __syncthreads();
+  if (warp == 0) {  // exclusive scan of the 32 (item, warp) counts, one per lane
+    int32_t* flat = &s_cnt[0][0];
+    const int c = flat[lane];
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    flat[lane] = incl - c;
+    const long long agg = __shfl_sync(0xffffffffu, incl, 31);
+    const long long excl = decoupled_lookback(status, tile, agg, lane);
+    if (lane == 0) {
+      s_prefix = excl;
+      if (tile == ntiles - 1) hdr->n_bwd = excl + agg;
+    }
+  }
+  __syncthreads();
+  const long long pfx = s_prefix;
+  const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int it = 0; it < KEEP_ITEMS; ++it) {
+    const uint32_t b = __ballot_sync(0xffffffffu, (kbits >> it) & 1u);
+    if ((kbits >> it) & 1u) {
+      const int64_t r = base + static_cast<int64_t>(it) * DZ_THREADS;
+      const long long o = pfx + s_cnt[it][warp] + __popc(b & lt);
+      keep[o] = static_cast<int32_t>(r);
+      oidx2[o] = active_idx[r];
+    }
+  }
+}
+
+// dZ rows from the q tiles. Dense mode (keep == NULL): in place, row r of the
+// dZ buffer from q row r (zeros when g_r = 0). Skip mode: row r2 < n_bwd of
+// the packed buffer dz_out from q row keep[r2] (and Hc2[r2] = Hc[keep[r2]]),
+// rows [n_bwd, n_bwd rounded up to the tile) zeroed.
+__global__ void __launch_bounds__(DZ_THREADS)
+k_dz_from_q(const uint4* q_in, uint4* dz_out, int64_t ld_vec, int32_t V, int64_t n_vt,
             const float* __restrict__ pm, const float* __restrict__ lse_c,
             const float* __restrict__ g_c, const float* __restrict__ zy,
             const int32_t* __restrict__ tgt_c, int64_t y_off, float inv_temp,
-            const WsHeader* __restrict__ hdr, int64_t Rp) {
-  const int64_t T = hdr->n_active;
+            const WsHeader* __restrict__ hdr, int64_t Rp, const int32_t* __restrict__ keep,
+            const uint4* __restrict__ hc, uint4* __restrict__ hc2, int32_t h_vec) {
+  const int64_t r2 = blockIdx.x;
+  const int64_t T = keep ? hdr->n_bwd : hdr->n_active;
   const int64_t Tp = (T + 2 * TC_BM - 1) / (2 * TC_BM) * (2 * TC_BM);  // rows the GEMMs read
+  if (r2 >= Tp || r2 >= Rp) return;
   const int64_t nvec = (static_cast<int64_t>(V) + 7) / 8;   // 8 bf16 per 16-B vector
-  const int64_t r = blockIdx.x;
-  if (r >= Tp || r >= Rp) return;
-  uint4* row = dz + r * ld_vec;
-  const float g = r < T ? g_c[r] : 0.f;
+  uint4* row = dz_out + r2 * ld_vec;
+  const int64_t r = r2 < T ? (keep ? static_cast<int64_t>(keep[r2]) : r2) : -1;
+  const float g = r >= 0 ? g_c[r] : 0.f;
+  if (keep) {  // Hc row of the packed backward rows (zeros past n_bwd)
+    uint4* dst = hc2 + r2 * h_vec;
+    if (r >= 0) {
+      const uint4* src = hc + r * h_vec;
+      for (int i = threadIdx.x; i < h_vec; i += DZ_THREADS) dst[i] = src[i];
+    } else {
+      for (int i = threadIdx.x; i < h_vec; i += DZ_THREADS) dst[i] = make_uint4(0, 0, 0, 0);
+    }
+  }
   if (g == 0.f) {                                          // no gradient: dZ row = 0
     const uint4 z = make_uint4(0, 0, 0, 0);
     for (int64_t i = threadIdx.x; i < nvec; i += DZ_THREADS) row[i] = z;
     return;
   }
+  const uint4* qrow = q_in + r * ld_vec;
   const float coef = inv_temp * g;
   const float lse = lse_c[r];
   const int64_t yl = static_cast<int64_t>(tgt_c[r]) - y_off;
@@ -49,7 +130,7 @@ k_dz_from_q(uint4* __restrict__ dz, int64_t ld_vec, int32_t V, int64_t n_vt,
   for (int64_t i = threadIdx.x; i < nvec; i += DZ_THREADS) {
     const int64_t v = i >> 5;                                // 32 vectors per vocab tile
     const float sc = -coef * __expf(pmr[v * 32] - lse);      // -tau^-1 g e^{m_rv - lse}
-    uint4 q = row[i];
+    uint4 q = qrow[i];
     uint32_t* w = reinterpret_cast<uint32_t*>(&q);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -67,18 +148,33 @@ k_dz_from_q(uint4* __restrict__ dz, int64_t ld_vec, int32_t V, int64_t n_vt,
   }
 }
 
-rl_status launch_dz_from_q(const rl_head* hd, const WsLayout& L, char* ws, cudaStream_t s) {
+rl_status launch_dz_from_q(const rl_head* hd, const WsLayout& L, char* ws, cudaStream_t s,
+                           bool skip_zero_rows) {
   if (L.Rp <= 0) return RL_OK;
+  WsHeader* hdr = reinterpret_cast<WsHeader*>(ws + L.off_hdr);
+  int32_t* keep = nullptr;
+  if (skip_zero_rows) {
+    keep = reinterpret_cast<int32_t*>(ws + L.off_keep);
+    const int64_t ntiles = ceil_div(L.Rp, DZ_THREADS * KEEP_ITEMS);
+    TraceScope ts(RL_K_DZQ, s);
+    k_keep_compact<<<static_cast<unsigned>(ntiles), DZ_THREADS, 0, s>>>(
+        reinterpret_cast<const float*>(ws + L.off_g),
+        reinterpret_cast<const int32_t*>(ws + L.off_active), hdr,
+        reinterpret_cast<unsigned long long*>(ws + L.off_st2), ntiles, keep,
+        reinterpret_cast<int32_t*>(ws + L.off_oidx2));
+    RLH_CHECK_LAUNCH();
+  }
   TraceScope ts(RL_K_DZQ, s);
-  // one CTA per row (a bounded persistent grid, which would leave room for a
-  // GEMM CTA of another micro-batch beside it, measured 1.7x slower alone)
   k_dz_from_q<<<static_cast<unsigned>(L.Rp), DZ_THREADS, 0, s>>>(
-      reinterpret_cast<uint4*>(ws + L.off_dz), L.Vp / 8, hd->vocab, L.n_vt,
-      reinterpret_cast<const float*>(ws + L.off_pm), reinterpret_cast<const float*>(ws + L.off_lse),
-      reinterpret_cast<const float*>(ws + L.off_g), reinterpret_cast<const float*>(ws + L.off_zy),
+      reinterpret_cast<const uint4*>(ws + L.off_dz),
+      reinterpret_cast<uint4*>(ws + (skip_zero_rows ? L.off_dz2 : L.off_dz)), L.Vp / 8,
+      hd->vocab, L.n_vt, reinterpret_cast<const float*>(ws + L.off_pm),
+      reinterpret_cast<const float*>(ws + L.off_lse), reinterpret_cast<const float*>(ws + L.off_g),
+      reinterpret_cast<const float*>(ws + L.off_zy),
       reinterpret_cast<const int32_t*>(ws + L.off_tgt),
-      hd->vocab_total > 0 ? hd->vocab_offset : 0, hd->inv_temperature,
-      reinterpret_cast<const WsHeader*>(ws + L.off_hdr), L.Rp);
+      hd->vocab_total > 0 ? hd->vocab_offset : 0, hd->inv_temperature, hdr, L.Rp, keep,
+      reinterpret_cast<const uint4*>(ws + L.off_hc), reinterpret_cast<uint4*>(ws + L.off_hc2),
+      hd->hidden / 8);
   RLH_CHECK_LAUNCH();
   return RL_OK;
 }

@@ -16,8 +16,9 @@ rl_status launch_prepare(const rl_head* hd, const rl_batch* b, const WsLayout& L
 rl_status launch_gather_bf16(const rl_head* hd, const void* hidden, const WsLayout& L, char* ws,
                              cudaStream_t s);
 // grad_hidden rows of inactive rows := 0.
+// all_rows: zero every row (skip mode: dH writes only the rows with g != 0).
 rl_status launch_zero_inactive(const rl_head* hd, void* grad_hidden, const WsLayout& L, char* ws,
-                               cudaStream_t s, bool f32_rows = false);
+                               cudaStream_t s, bool f32_rows = false, bool all_rows = false);
 
 // H2 GRPO.
 rl_status launch_grpo(const float* rewards, const int32_t* gos, int32_t S, int32_t G,
@@ -81,18 +82,26 @@ rl_status launch_simt_bwd(const rl_head* hd, const void* hidden, const void* wei
 // Tensor-core path (bf16, tcgen05/TMEM/TMA).
 // q_out: the epilogue also stores q = e^{z - m_tile} (bf16, 0 at the target)
 // into the dZ buffer for launch_dz_from_q.
+// q_adv (with q_out): advantages per sequence (per packed row if
+// q_adv_per_row); a warp's 32 rows that all have A = 0 store no q (skip mode
+// never reads them back). NULL: store every box.
 rl_status launch_tc_fwd(const rl_head* hd, const void* weight, const WsLayout& L, char* ws,
-                        cudaStream_t s, bool q_out = false);
+                        cudaStream_t s, bool q_out = false, const float* q_adv = nullptr,
+                        bool q_adv_per_row = false);
 // dZ = tau^-1 g (onehot - p) in place over the q tiles of launch_tc_fwd(q_out):
 // p = q e^{m_tile - lse} off the target, 1 - p_y = -expm1(z_y - lse) at it.
-rl_status launch_dz_from_q(const rl_head* hd, const WsLayout& L, char* ws, cudaStream_t s);
+// skip_zero_rows: pack the rows with dL/dlogp != 0 first (hdr->n_bwd) and
+// write their dZ / Hc rows densely into the dz2 / hc2 buffers for the
+// backward GEMMs (rows with g = 0 contribute exactly nothing).
+rl_status launch_dz_from_q(const rl_head* hd, const WsLayout& L, char* ws, cudaStream_t s,
+                           bool skip_zero_rows = false);
 // grad_hidden_f32 != NULL: dL/dH as fp32 rows [R, hidden] there instead of
 // bf16 rows into grad_hidden; gh_multicast: grad_hidden_f32 is an NVLS
 // multicast address and the rows are added into every rank's copy.
 rl_status launch_tc_bwd(const rl_head* hd, const void* weight, void* grad_hidden,
                         float* grad_hidden_f32, bool gh_multicast, float* grad_weight,
                         const rl_peer_group* dw_rs, bool entropy_on, const WsLayout& L, char* ws,
-                        cudaStream_t s, bool dz_ready = false);
+                        cudaStream_t s, bool dz_ready = false, bool skip_rows = false);
 
 int num_sms();
 

@@ -19,7 +19,8 @@ static_assert(PREP_THREADS * PREP_ITEMS_SMALL == H1_TILE_ROWS, "workspace status
 // claim counter, GEMM tile schedulers) and the scan's tile status words.
 __global__ void __launch_bounds__(1024)
 k_validate(const int32_t* __restrict__ cu, int32_t S, int64_t R, WsHeader* hdr,
-           unsigned long long* __restrict__ status, int64_t ntiles, int32_t* err) {
+           unsigned long long* __restrict__ status, int64_t ntiles,
+           unsigned long long* __restrict__ status2, int64_t ntiles2, int32_t* err) {
   int bad = 0;
   for (int64_t i = threadIdx.x; i <= S; i += blockDim.x) {
     const int32_t c = cu[i];
@@ -29,11 +30,15 @@ k_validate(const int32_t* __restrict__ cu, int32_t S, int64_t R, WsHeader* hdr,
     if (c < 0 || static_cast<int64_t>(c) > R) bad = 1;
   }
   for (int64_t i = threadIdx.x; i < ntiles; i += blockDim.x) status[i] = 0ull;
+  if (status2)
+    for (int64_t i = threadIdx.x; i < ntiles2; i += blockDim.x) status2[i] = 0ull;
   bad = __syncthreads_or(bad);
   if (threadIdx.x == 0) {
     hdr->bad_cu = bad;
     hdr->n_active = 0;
     hdr->tile_ctr = 0u;
+    hdr->n_bwd = 0;
+    hdr->tile_ctr2 = 0u;
     if (bad && err) atomicOr(err, RL_DEVERR_CU_SEQLENS);
   }
   if (threadIdx.x < 16) hdr->sched[threadIdx.x >> 1][threadIdx.x & 1] = 0u;
@@ -48,17 +53,6 @@ __device__ __forceinline__ int32_t upper_bound_i32(const int32_t* __restrict__ c
     if (static_cast<int64_t>(__ldg(cu + mid)) <= t) lo = mid + 1; else hi = mid;
   }
   return lo;
-}
-
-// Decoupled look-back status word of a tile: flag in the top 2 bits.
-constexpr unsigned long long ST_AGG = 1ull << 62;   // this tile's count only
-constexpr unsigned long long ST_PFX = 2ull << 62;   // inclusive prefix through this tile
-constexpr unsigned long long ST_VAL = (1ull << 62) - 1;
-
-__device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
 }
 
 // Launch 2 of 2 (single pass): per row the active flag (mask set, target in
@@ -164,32 +158,7 @@ k_flags_compact(const int32_t* __restrict__ cu, int32_t S, int64_t R,
       run += c4[k];
     }
     const long long agg = __shfl_sync(0xffffffffu, incl, 31);
-    // decoupled look-back
-    long long excl = 0;
-    if (tile == 0) {
-      if (lane == 0) atomicExch(status, ST_PFX | static_cast<unsigned long long>(agg));
-    } else {
-      if (lane == 0) atomicExch(status + tile, ST_AGG | static_cast<unsigned long long>(agg));
-      int64_t j = tile - 1;
-      while (true) {
-        const int64_t idx = j - lane;
-        unsigned long long v = ST_PFX;  // before tile 0: prefix 0
-        if (idx >= 0) {
-          do {
-            v = ld_volatile_u64(status + idx);
-          } while ((v >> 62) == 0ull);
-        }
-        const uint32_t pm = __ballot_sync(0xffffffffu, (v >> 62) == 2ull);
-        const int stop = pm ? __ffs(pm) - 1 : 31;  // nearest predecessor with a prefix
-        long long x = lane <= stop ? static_cast<long long>(v & ST_VAL) : 0ll;
-        x = warp_sum(x);
-        excl += x;
-        if (pm) break;
-        j -= 32;
-      }
-      if (lane == 0)
-        atomicExch(status + tile, ST_PFX | static_cast<unsigned long long>(excl + agg));
-    }
+    const long long excl = decoupled_lookback(status, tile, agg, lane);
     if (lane == 0) {
       s_prefix = excl;
       s_tile_total = agg;
@@ -263,8 +232,13 @@ rl_status launch_prepare(const rl_head* hd, const rl_batch* b, const WsLayout& L
   const int64_t ntiles = ceil_div(R, PREP_THREADS * items);
   {
     TraceScope ts(RL_K_PREPARE, s);
-    k_validate<<<1, 1024, 0, s>>>(b->cu_seqlens, b->num_seqs, R, hdr, status, ntiles,
-                                  b->err_flags);
+    // the backward-row compaction's status words (loss calls on the tensor-
+    // core path; absent when rl_batch_prepare's workspace prefix is all there is)
+    const bool st2 = L.off_st2 < L.off_dz2 && L.off_st2 + 8 <= L.total;
+    k_validate<<<1, 1024, 0, s>>>(
+        b->cu_seqlens, b->num_seqs, R, hdr, status, ntiles,
+        st2 ? reinterpret_cast<unsigned long long*>(ws + L.off_st2) : nullptr,
+        st2 ? ceil_div(L.Rp, H1_TILE_ROWS) : 0, b->err_flags);
   }
   RLH_CHECK_LAUNCH();
   if (ntiles > 0) {
@@ -338,7 +312,7 @@ k_zero_inactive(char* __restrict__ out, int64_t ld_bytes, int64_t row_bytes, int
                 const uint8_t* __restrict__ act) {
   const int64_t t = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
-  if (t >= R || act[t]) return;
+  if (t >= R || (act && act[t])) return;
   char* row = out + t * ld_bytes;
   if ((row_bytes & 15) == 0 && (reinterpret_cast<uintptr_t>(row) & 15) == 0) {
     uint4* v = reinterpret_cast<uint4*>(row);
@@ -350,8 +324,8 @@ k_zero_inactive(char* __restrict__ out, int64_t ld_bytes, int64_t row_bytes, int
 }
 
 rl_status launch_zero_inactive(const rl_head* hd, void* grad_hidden, const WsLayout& L, char* ws,
-                               cudaStream_t s, bool f32_rows) {
-  const uint8_t* act = reinterpret_cast<const uint8_t*>(ws + L.off_flags);
+                               cudaStream_t s, bool f32_rows, bool all_rows) {
+  const uint8_t* act = all_rows ? nullptr : reinterpret_cast<const uint8_t*>(ws + L.off_flags);
   const int64_t esz = (hd->dtype == RL_BF16 && !f32_rows) ? 2 : 4;
   const int64_t ld = f32_rows ? hd->hidden : hd->ld_hidden;
   const int64_t blocks = ceil_div(L.R, 8);

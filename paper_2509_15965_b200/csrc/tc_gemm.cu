@@ -123,6 +123,11 @@ struct TcArgs {
   // staging buffer over NVLink (plain stores; the owner sums the slots in
   // rank order afterwards, so the result is deterministic).
   int32_t dz_tma;      // EPI_DZ: stage bf16 32x32 boxes in smem, TMA-store them (tmA2 = dZ map)
+  int32_t dyn_bwd;     // m_dyn / k_dyn read the backward-row count (hdr->n_bwd, skip mode)
+  // q stores are skipped for a warp's 32 rows when every one has advantage 0
+  // (no gradient, never read back in skip mode); NULL = store every box
+  const float* q_adv;  // advantages, per sequence (seq_c) or per packed row (active_idx)
+  const int32_t* q_row;  // seq_c or active_idx
   int32_t q_tma;       // EPI_LSE: also store q = e^{z - m_tile} (0 at the target) as bf16
                        // 32x32 boxes by TMA (tmA2 = map of the dZ buffer): the backward then
                        // needs no logits recompute (k_dz_from_q rescales q into dZ in place)
@@ -238,7 +243,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   // Tile space: problem 0, then (EPI_BWD only) problem 1 -- the dH and dW
   // GEMMs of one backward in a single persistent launch, so the short last
   // wave of one fills with tiles of the other.
-  const int64_t T = args.hdr->n_active;
+  const int64_t T = args.dyn_bwd ? args.hdr->n_bwd : args.hdr->n_active;
   Prob P0, P1;
   P0.init(args.m_dyn ? T : args.M, args.k_dyn ? T : args.K, C::TILE_M, args.n_tiles, args.group_m,
           EPI == EPI_ACC && args.rs_world > 0);
@@ -491,6 +496,9 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         const uint64_t st_pol = l2_policy_evict_first();
         const float m2 = m * LOG2E, sc2 = args.inv_temp * LOG2E;
         float u2 = 0.f;                  // sum e (z - m) log2 e
+        bool skip_q = false;             // warp-uniform
+        if (args.q_tma && args.q_adv)
+          skip_q = __all_sync(0xffffffffu, !row_ok || args.q_adv[args.q_row[row]] == 0.f);
 #pragma unroll 1
         for (int c = 0; c < TC_BN / 32; ++c) {
           uint32_t v[32];
@@ -516,7 +524,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
               u2 = fmaf(e[j], d2, u2);
             }
           }
-          if (!args.q_tma) continue;     // forward only: partials, no q
+          if (!args.q_tma || skip_q) continue;  // forward only / all-A = 0 rows: no q
           const int yc = yrel - c * 32;
           if (yc >= 0 && yc < 32) {
 #pragma unroll
@@ -972,7 +980,7 @@ static TcArgs base_args(const rl_head* hd, const WsLayout& L, char* ws) {
 }
 
 rl_status launch_tc_fwd(const rl_head* hd, const void* weight, const WsLayout& L, char* ws,
-                        cudaStream_t s, bool q_out) {
+                        cudaStream_t s, bool q_out, const float* q_adv, bool q_adv_per_row) {
   const int h = hd->hidden, V = hd->vocab;
   const int cg = tc_cta_group();
   CUtensorMap ma, mb;
@@ -993,6 +1001,8 @@ rl_status launch_tc_fwd(const rl_head* hd, const void* weight, const WsLayout& L
   CUtensorMap mq;
   if (q_out) {  // q tiles into the dZ buffer [Rp, Vp] (bf16, 32x32 TMA store boxes)
     t.q_tma = 1;
+    t.q_adv = q_adv;
+    t.q_row = reinterpret_cast<const int32_t*>(ws + (q_adv_per_row ? L.off_active : L.off_seq));
     if (!make_map_bf16_32(&mq, ws + L.off_dz, V, L.Rp, static_cast<uint64_t>(L.Vp) * 2))
       return RL_ERR_CUDA;
   }
@@ -1002,10 +1012,12 @@ rl_status launch_tc_fwd(const rl_head* hd, const void* weight, const WsLayout& L
 rl_status launch_tc_bwd(const rl_head* hd, const void* weight, void* grad_hidden,
                         float* grad_hidden_f32, bool gh_multicast, float* grad_weight,
                         const rl_peer_group* dw_rs, bool entropy_on, const WsLayout& L, char* ws,
-                        cudaStream_t s, bool dz_ready) {
+                        cudaStream_t s, bool dz_ready, bool skip_rows) {
   const int h = hd->hidden, V = hd->vocab;
   const int cg = tc_cta_group();
-  __nv_bfloat16* dz = reinterpret_cast<__nv_bfloat16*>(ws + L.off_dz);
+  // skip mode: dZ / Hc rows of the backward rows only (packed by k_dz_from_q)
+  __nv_bfloat16* dz = reinterpret_cast<__nv_bfloat16*>(ws + (skip_rows ? L.off_dz2 : L.off_dz));
+  char* hc_b = ws + (skip_rows ? L.off_hc2 : L.off_hc);
   rl_status st;
   // N5: recompute logits, dZ = tau^-1 g (onehot - p) -> bf16 [Rp, Vp] (unless
   // k_dz_from_q already built dZ from the forward's q tiles).
@@ -1045,7 +1057,7 @@ rl_status launch_tc_bwd(const rl_head* hd, const void* weight, void* grad_hidden
   if (!make_map(&ma6, dz, V, L.Rp, static_cast<uint64_t>(L.Vp) * 2, TC_BM) ||
       !make_map(&mb6, weight, h, V, static_cast<uint64_t>(h) * 2, 64) ||
       !make_map(&ma7, dz, V, L.Rp, static_cast<uint64_t>(L.Vp) * 2, 64) ||
-      !make_map(&mb7, ws + L.off_hc, h, L.Rp, static_cast<uint64_t>(h) * 2, 64))
+      !make_map(&mb7, hc_b, h, L.Rp, static_cast<uint64_t>(h) * 2, 64))
     return RL_ERR_CUDA;
   TcArgs t6 = base_args(hd, L, ws);
   t6.M = L.Rp;
@@ -1056,12 +1068,14 @@ rl_status launch_tc_bwd(const rl_head* hd, const void* weight, void* grad_hidden
   t6.ld_out = hd->ld_hidden;
   t6.out_f32 = grad_hidden_f32;
   t6.out_mc = gh_multicast ? 1 : 0;
-  t6.row_idx = reinterpret_cast<const int32_t*>(ws + L.off_active);
+  t6.row_idx = reinterpret_cast<const int32_t*>(ws + (skip_rows ? L.off_oidx2 : L.off_active));
+  t6.dyn_bwd = skip_rows ? 1 : 0;
   kind_policy(t6, "RLHEAD_L2_DH", -1);
   // serpentine K for dH measured neutral (~6 waves per micro-batch): off
   t6.k_serp = env_int("RLHEAD_DH_SERP", 0);
   use_sched(t6, ws, L, 2);
   TcArgs t7 = base_args(hd, L, ws);
+  t7.dyn_bwd = skip_rows ? 1 : 0;
   t7.M = V;
   t7.K = L.Rp;
   t7.k_dyn = 1;

@@ -247,6 +247,7 @@ class PolicyLossStep:
             self.grad_w = torch.zeros(weight.shape[0], weight.shape[1], dtype=torch.float32,
                                       device=dev)
         self.stats = R.new_stats(dev)
+        self.stats_local = R.new_stats(dev)
         self.logp = torch.empty(max(db.num_rows, 1), dtype=torch.float32, device=dev)
         self.entropy = (torch.empty(max(db.num_rows, 1), dtype=torch.float32, device=dev)
                         if want_entropy else None)
@@ -335,6 +336,7 @@ class PolicyLossStep:
         else:
             all_reduce_(self.grad_w, "sum", self.group)
         tm.record("dw_reduce")
+        self.stats_local.copy_(self.stats)    # this rank's own sums (for reporting)
         reduce_stats_(self.stats, self.group)
         tm.record("stats_gather")
         return self.stats

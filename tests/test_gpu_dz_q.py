@@ -114,3 +114,67 @@ def test_dz_from_q_vs_oracle(rl, seed, tau):
     assert (dH_q[lay.mask == 0] == 0).all()
     assert np.all(np.linalg.norm(ref["dH"], axis=1)[~nz] == 0)
     assert np.all(dH_q[~nz] == 0)
+
+
+def _env_run(rl, env, fn):
+    saved = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        return fn()
+    finally:
+        for k, v in saved.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+def test_backward_row_skip(rl):
+    """Skip mode (default): the backward GEMMs run only over rows with
+    dL/dlogp != 0 (GRPO groups with A = 0 here). dL/dH is bit-identical to the
+    dense backward (each output row is the same dot products), dW equal to
+    fp32 reassociation (the zero rows no longer share k-blocks), and both
+    match the oracle; with a KL term (beta > 0) the A = 0 rows keep a gradient
+    and must be kept."""
+    import torch
+    from workload import make_layout, make_tensors_torch, HeadConfig
+    cfg = HeadConfig("skip-bf16", 256, 3000, 10, 4, 200, "bf16", "reasoning")
+    lay = make_layout(cfg, seed=5)
+    adv, _ = oracle.grpo_advantage(lay.rewards, lay.group_of_seq, lay.num_groups)
+    assert (adv == 0).sum() >= 8 and (adv != 0).sum() >= 8     # forced A = 0 groups present
+    H, W = make_tensors_torch(cfg, lay.num_rows, seed=5)
+    fwd = oracle.logprob_fwd(H, W, lay.cu_seqlens, lay.mask, lay.targets)
+    old = guarded_old_logp(fwd["logp"], np.random.default_rng(5))
+    ref_lp = (fwd["logp"] + np.random.default_rng(6).normal(0, 0.3, lay.num_rows)).astype(np.float32)
+    d = dev_tensors(lay)
+    head = rl.Head(cfg.hidden, cfg.vocab, "bf16")
+    for kl in (0.0, 0.05):
+        def run():
+            logp = torch.empty(lay.num_rows, device="cuda")
+            gh = torch.full((lay.num_rows, cfg.hidden), 3.0, dtype=torch.bfloat16, device="cuda")
+            gw = torch.zeros(cfg.vocab, cfg.hidden, device="cuda")
+            p = rl.LossParams(kl_coef=kl, ref_logp=torch.as_tensor(ref_lp, device="cuda"),
+                              n_tokens_global=torch.tensor([lay.num_tokens], device="cuda"))
+            tr = rl.Trace(64).start()
+            rl.rl_policy_loss_fwd_bwd(head, H.cuda(), W.cuda(),
+                                      rl.Batch(d["cu"], d["targets"], d["mask"]),
+                                      torch.as_tensor(old, dtype=torch.float32, device="cuda"),
+                                      torch.as_tensor(adv, dtype=torch.float32, device="cuda"),
+                                      p, logp, gh, gw)
+            torch.cuda.synchronize()
+            tr.stop()
+            return gh.cpu(), gw.cpu().double()
+        gh_s, gw_s = _env_run(rl, {"RLHEAD_BWD_SKIP": "1"}, run)
+        gh_d, gw_d = _env_run(rl, {"RLHEAD_BWD_SKIP": "0"}, run)
+        assert torch.equal(gh_s, gh_d), kl
+        assert float((gw_s - gw_d).norm() / gw_d.norm()) <= 1e-5, kl
+        ref = oracle.policy_loss_fwd_bwd(H, W, lay.cu_seqlens, lay.mask, lay.targets, old, adv,
+                                         oracle.LossParams(kl_coef=kl), n_global=lay.num_tokens,
+                                         ref_logp=ref_lp.astype(np.float64))
+        dH = gh_s.double().numpy()
+        assert rel_fro(dH, ref["dH"]) <= 1e-2 and max_rel(dH, ref["dH"]) <= 1e-2
+        assert rel_fro(gw_s.numpy(), ref["dW"]) <= 1e-2
+        zero = np.all(ref["dH"] == 0, axis=1)
+        assert np.all(dH[zero] == 0)
+        if kl == 0.0:
+            assert zero[lay.mask.astype(bool)].sum() >= 50   # A = 0 rows really skipped

@@ -457,6 +457,10 @@ def main():
             "step_executed_tflops": round(step_tflops_exec / world, 1),
             "step_executed_frac_burst": round(step_tflops_exec / world / pk["bf16"], 4),
             "step_algorithmic_frac_burst": round(step_tflops_alg / world / pk["bf16"], 4)}
+    if skip:
+        roof["algorithmic_note"] = ("6hV per token counts the dH/dW work of the rows whose "
+                                    "dL/dlogp is exactly 0, which skip mode does not execute; "
+                                    "step_executed_* is the hardware's share")
 
     # ------------------------------------ auxiliary measurements (M.1, M.4)
     aux = None

@@ -136,7 +136,7 @@ k_grpo_seg(const float* __restrict__ r, const int32_t* __restrict__ gos, int32_t
     const int i0 = w * per, i1 = min(S, i0 + per);
     GStat* my = acc + static_cast<int64_t>(w) * G;
     GStat* st = stg + w * 32;
-    constexpr int U = 8;                 // steps whose loads are issued together
+    constexpr int U = 2;  // steps whose loads are issued together (code size: one cold CTA)
     for (int b0 = i0; b0 < i1; b0 += 32 * U) {
       int32_t gk[U];
       float rk[U];
@@ -202,7 +202,8 @@ k_grpo_seg(const float* __restrict__ r, const int32_t* __restrict__ gos, int32_t
       t = {sum_in[3 * g], sum_in[3 * g + 1], sum_in[3 * g + 2], max_in[2 * g], max_in[2 * g + 1]};
     } else {
       t = acc[g];
-      for (int k = 1; k < GSEG_WARPS; ++k) t = gstat_combine(t, acc[static_cast<int64_t>(k) * G + g]);
+      for (int k = 1; k < GSEG_WARPS; ++k)
+        t = gstat_combine(t, acc[static_cast<int64_t>(k) * G + g]);
     }
     if (sum_out) {
       sum_out[3 * g] = t.n;

@@ -61,15 +61,37 @@ def pack_micro_batches(seq_rows, budget: int):
     return out
 
 
-def shard_layout(layout, rank: int, world: int, split_groups: bool = False):
-    """This rank's sequences, LPT by response tokens: whole groups (advantages
-    rank-local), or with ``split_groups`` single sequences (finer balance; the
-    group statistics are then all-reduced)."""
+def group_has_gradient(layout):
+    """Per group: True unless all its rewards are equal -- a GRPO group whose
+    rewards are all equal has A = 0 for every member, so its tokens need the
+    forward only (the backward GEMMs skip rows with dL/dlogp = 0). A host-side
+    scheduling estimate, not numerics."""
+    G = layout.num_groups
+    r = np.asarray(layout.rewards, dtype=np.float64)
+    g = np.asarray(layout.group_of_seq, dtype=np.int64)
+    mx = np.full(G, -np.inf)
+    mn = np.full(G, np.inf)
+    np.maximum.at(mx, g, r)
+    np.minimum.at(mn, g, r)
+    return mx > mn
+
+
+def shard_layout(layout, rank: int, world: int, split_groups: bool = False,
+                 work_weighted: bool = True):
+    """This rank's sequences, LPT by work: whole groups (advantages rank-local),
+    or with ``split_groups`` single sequences (finer balance; the group
+    statistics are then all-reduced). The weight of a group is
+    its response tokens x 3 (forward 2hV + backward 4hV per token) when its
+    rewards differ, x 1 when they are all equal (A = 0: forward only, the
+    backward skips those rows); ``work_weighted=False`` weighs tokens only.
+    The returned loads are the weights, in those units."""
     G = layout.num_groups
     cu = layout.cu_seqlens.astype(np.int64)
     seq_tokens = np.add.reduceat(layout.mask.astype(np.int64), cu[:-1]) \
         if layout.num_rows else np.zeros(layout.num_seqs, np.int64)
     seq_tokens = np.where(cu[1:] > cu[:-1], seq_tokens, 0)
+    if work_weighted and G > 0:
+        seq_tokens = seq_tokens * np.where(group_has_gradient(layout)[layout.group_of_seq], 3, 1)
     if split_groups:
         bins, loads = lpt_shard(seq_tokens, world)
         return list(bins[rank]), loads

@@ -1,8 +1,8 @@
 #!/bin/bash
 # 4-GPU scaling on one box: Qwen-7B head and OpenVLA head at N = 1, 2, 4
 # (bench's own relaunch), per-phase times; the 2-rank DP-vs-oracle test.
-mkdir -p gpurun_out/r2_4gpu
-O=gpurun_out/r2_4gpu
+mkdir -p gpurun_out/${OUT:-r2_4gpu}
+O=gpurun_out/${OUT:-r2_4gpu}
 nvidia-smi topo -m > $O/topo.txt 2>&1
 for cfg in openvla qwen7b; do
   for n in 1 2 4; do

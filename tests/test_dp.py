@@ -165,10 +165,32 @@ def test_shard_layout_split_groups_partition():
     cu = lay.cu_seqlens.astype(np.int64)
     tok = np.add.reduceat(lay.mask.astype(np.int64), cu[:-1])
     for world in (2, 3, 8):
-        got = [shard_layout(lay, r, world, split_groups=True) for r in range(world)]
+        got = [shard_layout(lay, r, world, split_groups=True, work_weighted=False)
+               for r in range(world)]
         seqs = sorted(s for g, _ in got for s in g)
         assert seqs == list(range(lay.num_seqs))
         loads = got[0][1]
         assert loads.max() - loads.min() <= tok.max()
         for r, (g, _) in enumerate(got):
             assert int(tok[g].sum()) == int(loads[r])
+
+
+def test_shard_work_weighted():
+    """Default LPT weights: response tokens x 3 for groups whose rewards differ
+    (forward + backward), x 1 for all-equal groups (A = 0: the backward skips
+    their rows). Loads are those weights; whole groups; LPT bound holds."""
+    from paper_2509_15965_b200.dp import group_has_gradient, shard_layout
+    from workload import CONFIGS, make_layout
+    lay = make_layout(CONFIGS["qwen7b"], 0)
+    cu = lay.cu_seqlens.astype(np.int64)
+    tok = np.add.reduceat(lay.mask.astype(np.int64), cu[:-1])
+    hg = group_has_gradient(lay)
+    assert not hg[0] and not hg[1] and hg.sum() > lay.num_groups // 2   # forced A = 0 groups
+    w_g = np.bincount(lay.group_of_seq, weights=tok * np.where(hg[lay.group_of_seq], 3, 1),
+                      minlength=lay.num_groups)
+    for world in (2, 4, 8):
+        got = [shard_layout(lay, r, world) for r in range(world)]
+        loads = got[0][1]
+        for r, (seqs, _) in enumerate(got):
+            assert int(w_g[np.unique(lay.group_of_seq[seqs])].sum()) == int(loads[r])
+        assert loads.max() - loads.min() <= w_g.max()

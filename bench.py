@@ -57,6 +57,9 @@ def parse():
     p.add_argument("--collective", default="symm", choices=["symm", "nccl"],
                    help="N>1 dW reduction: reduce-scatter fused into the last dW GEMM epilogue "
                         "+ NVLink all-gather (symm), or NCCL all-reduce")
+    p.add_argument("--split-groups", type=int, default=0,
+                   help="N>1: LPT over single sequences (group statistics all-reduced) "
+                        "instead of whole groups -- finer balance for few large groups")
     p.add_argument("--pipeline", type=int, default=0,
                    help="1: two-stream micro-batch pipeline (bwd(i) beside fwd(i+1))")
     p.add_argument("--phases", action="store_true",
@@ -311,13 +314,14 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     layout = make_layout(cfg, seed=args.seed)
-    seqs, loads = shard_layout(layout, rank, world)
+    split = bool(args.split_groups) and world > 1
+    seqs, loads = shard_layout(layout, rank, world, split_groups=split)
     mine, _ = sub_layout(layout, seqs)
-    db = device_batch(mine, args.mb_rows, device=dev)
+    db = device_batch(mine, args.mb_rows, device=dev, global_groups=split)
     if args.max_mb:  # debug: the sequences of the first max_mb micro-batches only
         s_end = db.mbs[min(args.max_mb, len(db.mbs)) - 1][1]
         mine, _ = sub_layout(mine, np.arange(s_end))
-        db = device_batch(mine, args.mb_rows, device=dev)
+        db = device_batch(mine, args.mb_rows, device=dev, global_groups=split)
     _, W = make_tensors_torch(cfg, 0, seed=args.seed, device=dev, hidden=False)
     H, _ = make_tensors_torch(cfg, mine.num_rows, seed=args.seed + 7919 * (rank + 1), device=dev,
                               weight=False)
@@ -337,12 +341,12 @@ def main():
     try:
         step = PolicyLossStep(head, W, db, group=group,
                               collective="symm" if collective == "symm" else "nccl",
-                              pipeline=bool(args.pipeline))
+                              pipeline=bool(args.pipeline), split_groups=split)
     except Exception as e:  # symmetric memory unavailable: NCCL all-reduce instead
         print(f"[bench] collective=symm unavailable ({e}); using nccl", file=sys.stderr)
         collective = "nccl"
         step = PolicyLossStep(head, W, db, group=group, collective="nccl",
-                              pipeline=bool(args.pipeline))
+                              pipeline=bool(args.pipeline), split_groups=split)
     gh = torch.empty(max_mb, cfg.hidden, dtype=H.dtype, device=dev)
     tokens_local = int(sum(int(mine.mask[r0:r1].sum()) for _, _, r0, r1, _ in db.mbs))
     tok_t = torch.tensor([tokens_local], dtype=torch.int64, device=dev)
@@ -491,6 +495,7 @@ def main():
                        "global_batch_tokens": tokens_global, "micro_batch_rows": args.mb_rows,
                        "micro_batches_per_rank": len(db.mbs), "parallelism": f"dp{world}",
                        "dw_collective": collective, "pipeline": bool(args.pipeline),
+                       "sharding": "sequences (split groups)" if split else "whole groups",
                        "l2": "inputs > L2 (hidden rows of the mini-batch ~ "
                              f"{mine.num_rows * cfg.hidden * 2 / 1e9:.1f} GB per rank)",
                        "lpt_load_max_over_mean": round(float(loads.max() / loads.mean()), 4),

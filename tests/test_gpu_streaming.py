@@ -84,3 +84,44 @@ def test_scale_by_inverse_count(rl):
         ref = oracle.head.scale_by_inverse_count(x.cpu().numpy(), n)
         # fp32: 1/N rounded once, the product rounded once -> 2 ulp relative
         np.testing.assert_allclose(y.cpu().numpy(), ref, rtol=2 * 2 ** -23)
+
+
+def test_streaming_vs_oracle(rl):
+    """The streaming interface (micro-batches fed before N is known, deferred
+    1/N) against the CPU float64 oracle of the whole global batch:
+    dW, the statistics and every micro-batch's logp within the bf16 tolerances."""
+    import torch
+    from paper_2509_15965_b200.dp import StreamingPolicyLoss, device_batch
+    cfg = SMALL_BF16
+    lay = make_layout(cfg, seed=43)
+    H, W = make_tensors_host(cfg, lay.num_rows, seed=43)
+    adv, _ = oracle.grpo_advantage(lay.rewards, lay.group_of_seq, lay.num_groups)
+    fwd = oracle.logprob_fwd(H, W, lay.cu_seqlens, lay.mask, lay.targets)
+    from tests.gpu_util import guarded_old_logp
+    old = guarded_old_logp(fwd["logp"], np.random.default_rng(43))
+    ref = oracle.policy_loss_fwd_bwd(H, W, lay.cu_seqlens, lay.mask, lay.targets, old, adv,
+                                     n_global=lay.num_tokens)
+    dev = "cuda"
+    Hd, Wd = H.to(dev), W.to(dev)
+    head = rl.Head(cfg.hidden, cfg.vocab, cfg.dtype)
+    db = device_batch(lay, 2048, device=dev)
+    assert len(db.mbs) >= 3
+    old_t = torch.as_tensor(old, dtype=torch.float32, device=dev)
+    adv_t = torch.as_tensor(adv, dtype=torch.float32, device=dev)
+    s = StreamingPolicyLoss(head, Wd)
+    s.begin()
+    logp = torch.empty(lay.num_rows, device=dev)
+    gh = torch.empty_like(Hd)
+    for (s0, s1, r0, r1, cu_mb) in db.mbs:
+        b = rl.Batch(cu_mb, db.targets[r0:r1], db.mask[r0:r1], num_rows=r1 - r0)
+        s.feed(Hd[r0:r1], b, old_t[r0:r1], adv_t[s0:s1], logp[r0:r1], gh[r0:r1])
+    s.finish()
+    torch.cuda.synchronize()
+    st = rl.read_stats(s.stats)
+    assert st["tokens"] == ref["stats"]["tokens"]
+    assert st["loss_sum"] == pytest.approx(ref["stats"]["loss_sum"], rel=1e-2)
+    assert np.abs(logp.cpu().double().numpy() - ref["logp"]).max() <= 2e-3
+    gw = s.grad_w.cpu().double().numpy()
+    assert rel_fro(gw, ref["dW"]) <= 1e-2
+    # dL/dH of the streamed micro-batches is unscaled (loss_scale = 1): x 1/N
+    assert rel_fro(gh.cpu().double().numpy() / lay.num_tokens, ref["dH"]) <= 1e-2

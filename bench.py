@@ -46,6 +46,9 @@ def parse():
                         "profiles/r1/SUMMARY.md)")
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--max-mb", type=int, default=0, help="debug: first micro-batches only")
+    p.add_argument("--mb-offset", type=int, default=0,
+                   help="debug, with --max-mb: start at this micro-batch (the first ones hold "
+                        "the forced A = 0 groups)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample-tokens", type=int, default=512,
@@ -318,9 +321,11 @@ def main():
     seqs, loads = shard_layout(layout, rank, world, split_groups=split)
     mine, _ = sub_layout(layout, seqs)
     db = device_batch(mine, args.mb_rows, device=dev, global_groups=split)
-    if args.max_mb:  # debug: the sequences of the first max_mb micro-batches only
-        s_end = db.mbs[min(args.max_mb, len(db.mbs)) - 1][1]
-        mine, _ = sub_layout(mine, np.arange(s_end))
+    if args.max_mb:  # debug: the sequences of max_mb micro-batches only
+        i0 = min(args.mb_offset, len(db.mbs) - 1)
+        s_beg = db.mbs[i0][0]
+        s_end = db.mbs[min(i0 + args.max_mb, len(db.mbs)) - 1][1]
+        mine, _ = sub_layout(mine, np.arange(s_beg, s_end))
         db = device_batch(mine, args.mb_rows, device=dev, global_groups=split)
     _, W = make_tensors_torch(cfg, 0, seed=args.seed, device=dev, hidden=False)
     H, _ = make_tensors_torch(cfg, mine.num_rows, seed=args.seed + 7919 * (rank + 1), device=dev,

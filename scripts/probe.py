@@ -23,6 +23,9 @@ def main():
     ap.add_argument("--config", default="qwen7b")
     ap.add_argument("--rows", type=int, default=65536)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--mb-index", type=int, default=10,
+                    help="which micro-batch of the layout (the first ones belong to the "
+                         "forced A = 0 groups, whose rows the backward skips)")
     ap.add_argument("--fwd-only", action="store_true")
     ap.add_argument("--cublas", action="store_true", help="also time torch.matmul of the shapes")
     ap.add_argument("--sustain", type=float, default=0.0, help="seconds of warm-up load")
@@ -35,7 +38,8 @@ def main():
     cfg = CONFIGS[a.config]
     lay = make_layout(cfg, 0)
     cu = lay.cu_seqlens.astype(np.int64)
-    s0, s1 = pack_micro_batches(cu[1:] - cu[:-1], a.rows)[0]
+    mbs = pack_micro_batches(cu[1:] - cu[:-1], a.rows)
+    s0, s1 = mbs[min(a.mb_index, len(mbs) - 1)]
     mb, _ = sub_layout(lay, np.arange(s0, s1))
     dev = "cuda"
     H, W = make_tensors_torch(cfg, mb.num_rows, seed=0, device=dev)
@@ -66,7 +70,7 @@ def main():
         once()
         torch.cuda.synchronize()
     tok = int(mb.mask.sum())
-    out = {"config": a.config, "tokens": tok, "reps": a.reps}
+    out = {"config": a.config, "tokens": tok, "reps": a.reps, "micro_batch": int(a.mb_index)}
     shapes = {}
     if a.cublas:
         # library reference: cuBLAS (torch.matmul) for the same GEMM shapes,

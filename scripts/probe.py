@@ -47,8 +47,12 @@ def main():
     b = rl.Batch(torch.as_tensor(mb.cu_seqlens, device=dev), torch.as_tensor(mb.targets, device=dev),
                  torch.as_tensor(mb.mask, device=dev))
     R = mb.num_rows
-    old = torch.zeros(R, device=dev)
-    adv = torch.linspace(-1, 1, mb.num_seqs, device=dev)
+    # ratios near 1 (old = own log-probs + 0.01) and |A| = 1: every active row
+    # carries a gradient, so the backward GEMMs see all rows (no skip)
+    old = torch.empty(R, device=dev)
+    rl.rl_logprob_fwd(head, H, W, b, old)
+    old += 0.01
+    adv = torch.where(torch.arange(mb.num_seqs, device=dev) % 2 == 0, 1.0, -1.0)
     p = rl.LossParams(n_tokens_global=torch.tensor([lay.num_tokens], device=dev))
     logp = torch.empty(R, device=dev)
     gh = torch.empty_like(H)

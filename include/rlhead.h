@@ -97,7 +97,10 @@ typedef struct {
 
 /* Workspace bytes for a call on up to `num_rows` packed rows: want_bwd = 0
  * for rl_logprob_fwd / the vocab-parallel calls, 1 for rl_policy_loss_fwd_bwd
- * (+ _vp), 2 for rl_batch_prepare alone (bookkeeping only, ~21 B/row).
+ * (+ _fwd / _bwd / _vp), 2 for rl_batch_prepare alone (bookkeeping only,
+ * ~21 B/row). The backward's share on the tensor-core path is dominated by two
+ * bf16 [rows, V] buffers (the forward's q / dZ, and the dZ of the rows with a
+ * gradient packed densely): ~4 V B per row, ~10 GB at 16k rows and V = 152k.
  * 0 if the head or want_bwd is invalid. */
 RL_API size_t rl_workspace_size(const rl_head *hd, int64_t num_rows, int32_t want_bwd);
 

@@ -284,3 +284,37 @@ def test_determinism_and_invariants(rl):
                               stats=st)
     torch.cuda.synchronize()
     assert gw.abs().max().item() == 0 and rl.read_stats(st)["tokens"] == 0
+
+
+def test_strided_hidden_rows(rl):
+    """ld_hidden > hidden (rows of a wider buffer, e.g. a fused trunk output):
+    the same logp / dL/dH / dW bit for bit as contiguous rows, dL/dH written
+    with the same row stride, and the columns past `hidden` never touched."""
+    import torch
+    cfg = SMALL_BF16
+    lay, H, W = _bf16_case(cfg, seed=12)
+    d = dev_tensors(lay)
+    R, h, ld = lay.num_rows, cfg.hidden, cfg.hidden + 64
+    adv = np.linspace(-1, 1, lay.num_seqs).astype(np.float32)
+    adv[0] = 0.0                                      # a row set without gradient
+    old = torch.zeros(R, device="cuda")
+    rl.rl_logprob_fwd(rl.Head(h, cfg.vocab, "bf16"), H.cuda(), W.cuda(),
+                      rl.Batch(d["cu"], d["targets"], d["mask"]), old)
+    old += 0.02
+    res = []
+    for stride in (h, ld):
+        buf = torch.full((R, stride), 5.0, dtype=torch.bfloat16, device="cuda")
+        buf[:, :h] = H.cuda()
+        gbuf = torch.full((R, stride), -3.0, dtype=torch.bfloat16, device="cuda")
+        head = rl.Head(h, cfg.vocab, "bf16", ld_hidden=stride)
+        logp = torch.empty(R, device="cuda")
+        gw = torch.zeros(cfg.vocab, h, device="cuda")
+        rl.rl_policy_loss_fwd_bwd(head, buf, W.cuda(), rl.Batch(d["cu"], d["targets"], d["mask"]),
+                                  old, torch.as_tensor(adv, device="cuda"), rl.LossParams(), logp,
+                                  gbuf, gw)
+        torch.cuda.synchronize()
+        if stride > h:
+            assert bool((gbuf[:, h:] == -3.0).all())     # padding columns untouched
+        res.append((logp.cpu(), gbuf[:, :h].cpu(), gw.cpu()))
+    for a, b in zip(res[0], res[1]):
+        assert torch.equal(a, b)

@@ -49,6 +49,10 @@ static bool bwd_skip() {
   const char* e = std::getenv("RLHEAD_BWD_SKIP");
   return !(e && e[0] == '0');
 }
+static bool dz_fused() {
+  const char* e = std::getenv("RLHEAD_DZ_FUSED");
+  return e && e[0] == '1';
+}
 static bool dz_recompute() {
   const char* e = std::getenv("RLHEAD_DZ_RECOMPUTE");
   return e && e[0] == '1';
@@ -359,6 +363,12 @@ static rl_status loss_impl(const rl_head* hd, const void* hidden, const void* we
   // and padding rows have dZ = 0 and contribute exactly nothing to dH / dW.
   // RLHEAD_BWD_SKIP=0 keeps every active row.
   const bool skip_rows = q_mode && bwd_skip();
+  // fused backward (RLHEAD_DZ_FUSED=1; token-mean GRPO without KL): the rows
+  // of A = 0 sequences are moved behind the others before the forward, so the
+  // backward covers a prefix of the compact rows in place (no packed copies)
+  const bool fused_dz = skip_rows && dz_fused() && p->kl_coef == 0.f && !p->seq_mean &&
+                        !p->adv_per_token;
+  const int bwd_rows = fused_dz ? BWD_PREFIX : skip_rows ? BWD_PACKED : BWD_DENSE;
   if (!ws || ws_bytes < L.total) return RL_ERR_WORKSPACE;
   if (!aligned(ws, 256)) return RL_ERR_INVALID_ARG;
   const bool tc = use_tc(hd);
@@ -383,16 +393,17 @@ static rl_status loss_impl(const rl_head* hd, const void* hidden, const void* we
     if (zero_gh &&
         (st = launch_zero_inactive(hd, grad_hidden, L, w, s, gh_f32, skip_rows)) != RL_OK)
       return st;
-    if (q_mode && (st = launch_dz_from_q(hd, L, w, s, skip_rows)) != RL_OK) return st;
+    if (q_mode && (st = launch_dz_from_q(hd, L, w, s, bwd_rows)) != RL_OK) return st;
     if (tc)
       return launch_tc_bwd(hd, weight, gh_f32 ? nullptr : grad_hidden,
                            gh_f32 ? static_cast<float*>(grad_hidden) : nullptr, gh_mc,
-                           grad_weight, rs, entropy_on, L, w, s, q_mode, skip_rows);
+                           grad_weight, rs, entropy_on, L, w, s, q_mode, bwd_rows);
     return launch_simt_bwd(hd, hidden, weight, grad_hidden, grad_weight, entropy_on, L, w, s);
   }
   st = launch_prepare(hd, b, L, w, nullptr, nullptr, nullptr, nullptr, nullptr, logp, entropy,
                       nullptr, s);
   if (st != RL_OK) return st;
+  if (fused_dz && (st = launch_partition_rows(L, w, adv, s)) != RL_OK) return st;
   if (zero_gh &&
       (st = launch_zero_inactive(hd, grad_hidden, L, w, s, gh_f32, skip_rows)) != RL_OK)
     return st;
@@ -446,11 +457,11 @@ static rl_status loss_impl(const rl_head* hd, const void* hidden, const void* we
   if ((st = launch_merge(L, w, a, s)) != RL_OK) return st;
   if ((st = launch_stats_reduce(L, w, stats, s)) != RL_OK) return st;
   if (!(phase & 2)) return RL_OK;
-  if (q_mode && (st = launch_dz_from_q(hd, L, w, s, skip_rows)) != RL_OK) return st;
+  if (q_mode && (st = launch_dz_from_q(hd, L, w, s, bwd_rows)) != RL_OK) return st;
   if (tc)
     return launch_tc_bwd(hd, weight, gh_f32 ? nullptr : grad_hidden,
                          gh_f32 ? static_cast<float*>(grad_hidden) : nullptr, gh_mc,
-                         grad_weight, rs, entropy_on, L, w, s, q_mode, skip_rows);
+                         grad_weight, rs, entropy_on, L, w, s, q_mode, bwd_rows);
   return launch_simt_bwd(hd, hidden, weight, grad_hidden, grad_weight, entropy_on, L, w, s);
 }
 

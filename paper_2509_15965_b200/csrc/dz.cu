@@ -86,6 +86,115 @@ k_keep_compact(const float* __restrict__ g_c, const int32_t* __restrict__ active
   }
 }
 
+// Fused-backward mode (RLHEAD_DZ_FUSED=1): before the forward, reorder the
+// compact rows so the rows that can carry a gradient (their sequence's
+// advantage A != 0; no KL term) come first, in order, and the A = 0 rows fill
+// the tail (in reverse order): active_idx / tgt_c / seq_c are rewritten from
+// copies (src_*), hdr->n_bwd = the prefix length. The backward GEMMs then run
+// over that prefix of Hc / q in place. One pass: per tile the two classes'
+// counts, packed (c1 << 31 | c0) in one decoupled look-back word; T (the
+// active count, from H1) places the tail.
+__global__ void __launch_bounds__(DZ_THREADS)
+k_partition_rows(const int32_t* __restrict__ src_idx, const int32_t* __restrict__ src_tgt,
+                 const int32_t* __restrict__ src_seq, const float* __restrict__ adv,
+                 WsHeader* hdr, unsigned long long* status, int64_t ntiles,
+                 int32_t* __restrict__ active_idx, int32_t* __restrict__ tgt_c,
+                 int32_t* __restrict__ seq_c) {
+  __shared__ int32_t s_cnt[2][KEEP_ITEMS][DZ_THREADS / 32];
+  __shared__ long long s_p1, s_p0;
+  __shared__ int32_t s_tile;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_tile = static_cast<int32_t>(atomicAdd(&hdr->tile_ctr2, 1u));
+  __syncthreads();
+  const int64_t tile = s_tile;
+  const int64_t T = hdr->n_active;
+  const int64_t base = tile * (DZ_THREADS * KEEP_ITEMS) + tid;
+  uint32_t vbits = 0, cbits = 0;  // valid row / class 1 (A != 0)
+#pragma unroll
+  for (int it = 0; it < KEEP_ITEMS; ++it) {
+    const int64_t r = base + static_cast<int64_t>(it) * DZ_THREADS;
+    if (r < T) {
+      vbits |= 1u << it;
+      if (adv[src_seq[r]] != 0.f) cbits |= 1u << it;
+    }
+  }
+#pragma unroll
+  for (int it = 0; it < KEEP_ITEMS; ++it) {
+    const uint32_t b1 = __ballot_sync(0xffffffffu, (cbits >> it) & 1u);
+    const uint32_t b0 = __ballot_sync(0xffffffffu, ((vbits & ~cbits) >> it) & 1u);
+    if (lane == 0) {
+      s_cnt[1][it][warp] = __popc(b1);
+      s_cnt[0][it][warp] = __popc(b0);
+    }
+  }
+  __syncthreads();
+  if (warp == 0) {  // exclusive scans of the 32 (item, warp) counts of each class
+    int32_t* f1 = &s_cnt[1][0][0];
+    int32_t* f0 = &s_cnt[0][0][0];
+    const int c1 = f1[lane], c0 = f0[lane];
+    int i1 = c1, i0 = c0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v1 = __shfl_up_sync(0xffffffffu, i1, o);
+      const int v0 = __shfl_up_sync(0xffffffffu, i0, o);
+      if (lane >= o) {
+        i1 += v1;
+        i0 += v0;
+      }
+    }
+    f1[lane] = i1 - c1;
+    f0[lane] = i0 - c0;
+    const long long a1 = __shfl_sync(0xffffffffu, i1, 31);
+    const long long a0 = __shfl_sync(0xffffffffu, i0, 31);
+    const long long excl = decoupled_lookback(status, tile, (a1 << 31) | a0, lane);
+    if (lane == 0) {
+      s_p1 = excl >> 31;
+      s_p0 = excl & ((1ll << 31) - 1);
+      if (tile == ntiles - 1) hdr->n_bwd = s_p1 + a1;
+    }
+  }
+  __syncthreads();
+  const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int it = 0; it < KEEP_ITEMS; ++it) {
+    const uint32_t b1 = __ballot_sync(0xffffffffu, (cbits >> it) & 1u);
+    const uint32_t b0 = __ballot_sync(0xffffffffu, ((vbits & ~cbits) >> it) & 1u);
+    if ((vbits >> it) & 1u) {
+      const int64_t r = base + static_cast<int64_t>(it) * DZ_THREADS;
+      const bool c = (cbits >> it) & 1u;
+      const long long o = c ? s_p1 + s_cnt[1][it][warp] + __popc(b1 & lt)
+                            : T - 1 - (s_p0 + s_cnt[0][it][warp] + __popc(b0 & lt));
+      active_idx[o] = src_idx[r];
+      tgt_c[o] = src_tgt[r];
+      seq_c[o] = src_seq[r];
+    }
+  }
+}
+
+rl_status launch_partition_rows(const WsLayout& L, char* ws, const float* adv, cudaStream_t s) {
+  if (L.Rp <= 0) return RL_OK;
+  WsHeader* hdr = reinterpret_cast<WsHeader*>(ws + L.off_hdr);
+  int32_t* act = reinterpret_cast<int32_t*>(ws + L.off_active);
+  int32_t* tgt = reinterpret_cast<int32_t*>(ws + L.off_tgt);
+  int32_t* seq = reinterpret_cast<int32_t*>(ws + L.off_seq);
+  // sources: copies in the (unused in this mode) packed-row scratch of skip mode
+  int32_t* s_act = reinterpret_cast<int32_t*>(ws + L.off_keep);
+  int32_t* s_tgt = reinterpret_cast<int32_t*>(ws + L.off_oidx2);
+  int32_t* s_seq = reinterpret_cast<int32_t*>(ws + L.off_hc2);
+  const size_t nb = static_cast<size_t>(L.Rp) * 4;
+  if (cudaMemcpyAsync(s_act, act, nb, cudaMemcpyDeviceToDevice, s) != cudaSuccess ||
+      cudaMemcpyAsync(s_tgt, tgt, nb, cudaMemcpyDeviceToDevice, s) != cudaSuccess ||
+      cudaMemcpyAsync(s_seq, seq, nb, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+    return RL_ERR_CUDA;
+  const int64_t ntiles = ceil_div(L.Rp, DZ_THREADS * KEEP_ITEMS);
+  TraceScope ts(RL_K_PREPARE, s);
+  k_partition_rows<<<static_cast<unsigned>(ntiles), DZ_THREADS, 0, s>>>(
+      s_act, s_tgt, s_seq, adv, hdr, reinterpret_cast<unsigned long long*>(ws + L.off_st2),
+      ntiles, act, tgt, seq);
+  RLH_CHECK_LAUNCH();
+  return RL_OK;
+}
+
 // dZ rows from the q tiles. Dense mode (keep == NULL): in place, row r of the
 // dZ buffer from q row r (zeros when g_r = 0). Skip mode: row r2 < n_bwd of
 // the packed buffer dz_out from q row keep[r2] (and Hc2[r2] = Hc[keep[r2]]),
@@ -96,9 +205,10 @@ k_dz_from_q(const uint4* q_in, uint4* dz_out, int64_t ld_vec, int32_t V, int64_t
             const float* __restrict__ g_c, const float* __restrict__ zy,
             const int32_t* __restrict__ tgt_c, int64_t y_off, float inv_temp,
             const WsHeader* __restrict__ hdr, int64_t Rp, const int32_t* __restrict__ keep,
-            const uint4* __restrict__ hc, uint4* __restrict__ hc2, int32_t h_vec) {
+            const uint4* __restrict__ hc, uint4* __restrict__ hc2, int32_t h_vec,
+            int32_t use_nbwd) {
   const int64_t r2 = blockIdx.x;
-  const int64_t T = keep ? hdr->n_bwd : hdr->n_active;
+  const int64_t T = use_nbwd ? hdr->n_bwd : hdr->n_active;
   const int64_t Tp = (T + 2 * TC_BM - 1) / (2 * TC_BM) * (2 * TC_BM);  // rows the GEMMs read
   if (r2 >= Tp || r2 >= Rp) return;
   const int64_t nvec = (static_cast<int64_t>(V) + 7) / 8;   // 8 bf16 per 16-B vector
@@ -149,9 +259,10 @@ k_dz_from_q(const uint4* q_in, uint4* dz_out, int64_t ld_vec, int32_t V, int64_t
 }
 
 rl_status launch_dz_from_q(const rl_head* hd, const WsLayout& L, char* ws, cudaStream_t s,
-                           bool skip_zero_rows) {
+                           int bwd_rows) {
   if (L.Rp <= 0) return RL_OK;
   WsHeader* hdr = reinterpret_cast<WsHeader*>(ws + L.off_hdr);
+  const bool skip_zero_rows = bwd_rows == BWD_PACKED;
   int32_t* keep = nullptr;
   if (skip_zero_rows) {
     keep = reinterpret_cast<int32_t*>(ws + L.off_keep);
@@ -174,7 +285,7 @@ rl_status launch_dz_from_q(const rl_head* hd, const WsLayout& L, char* ws, cudaS
       reinterpret_cast<const int32_t*>(ws + L.off_tgt),
       hd->vocab_total > 0 ? hd->vocab_offset : 0, hd->inv_temperature, hdr, L.Rp, keep,
       reinterpret_cast<const uint4*>(ws + L.off_hc), reinterpret_cast<uint4*>(ws + L.off_hc2),
-      hd->hidden / 8);
+      hd->hidden / 8, bwd_rows != BWD_DENSE ? 1 : 0);
   RLH_CHECK_LAUNCH();
   return RL_OK;
 }

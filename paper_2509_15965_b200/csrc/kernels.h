@@ -90,18 +90,26 @@ rl_status launch_tc_fwd(const rl_head* hd, const void* weight, const WsLayout& L
                         bool q_adv_per_row = false);
 // dZ = tau^-1 g (onehot - p) in place over the q tiles of launch_tc_fwd(q_out):
 // p = q e^{m_tile - lse} off the target, 1 - p_y = -expm1(z_y - lse) at it.
-// skip_zero_rows: pack the rows with dL/dlogp != 0 first (hdr->n_bwd) and
-// write their dZ / Hc rows densely into the dz2 / hc2 buffers for the
-// backward GEMMs (rows with g = 0 contribute exactly nothing).
+// Which rows the backward GEMMs (and the dZ pass) cover:
+//  BWD_DENSE  every active row, dZ in place, Hc as gathered (hdr->n_active);
+//  BWD_PACKED the rows with dL/dlogp != 0, packed by k_keep_compact into the
+//             dz2 / hc2 buffers (hdr->n_bwd; rows with g = 0 add exactly nothing);
+//  BWD_PREFIX the prefix [0, hdr->n_bwd) of the compact rows after
+//             launch_partition_rows (A != 0 rows first): dZ in place, Hc as is.
+enum { BWD_DENSE = 0, BWD_PACKED = 1, BWD_PREFIX = 2 };
 rl_status launch_dz_from_q(const rl_head* hd, const WsLayout& L, char* ws, cudaStream_t s,
-                           bool skip_zero_rows = false);
+                           int bwd_rows = BWD_DENSE);
+// Fused-backward mode: reorder the compact rows (A != 0 first, A = 0 tail);
+// hdr->n_bwd = the prefix length. Run after H1, before the gather.
+rl_status launch_partition_rows(const WsLayout& L, char* ws, const float* adv, cudaStream_t s);
 // grad_hidden_f32 != NULL: dL/dH as fp32 rows [R, hidden] there instead of
 // bf16 rows into grad_hidden; gh_multicast: grad_hidden_f32 is an NVLS
 // multicast address and the rows are added into every rank's copy.
 rl_status launch_tc_bwd(const rl_head* hd, const void* weight, void* grad_hidden,
                         float* grad_hidden_f32, bool gh_multicast, float* grad_weight,
                         const rl_peer_group* dw_rs, bool entropy_on, const WsLayout& L, char* ws,
-                        cudaStream_t s, bool dz_ready = false, bool skip_rows = false);
+                        cudaStream_t s, bool dz_ready = false, int bwd_rows = BWD_DENSE,
+                        bool dz_convert = false);
 
 int num_sms();
 

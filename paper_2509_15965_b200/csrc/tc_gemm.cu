@@ -1012,12 +1012,13 @@ rl_status launch_tc_fwd(const rl_head* hd, const void* weight, const WsLayout& L
 rl_status launch_tc_bwd(const rl_head* hd, const void* weight, void* grad_hidden,
                         float* grad_hidden_f32, bool gh_multicast, float* grad_weight,
                         const rl_peer_group* dw_rs, bool entropy_on, const WsLayout& L, char* ws,
-                        cudaStream_t s, bool dz_ready, bool skip_rows) {
+                        cudaStream_t s, bool dz_ready, int bwd_rows, bool dz_convert) {
   const int h = hd->hidden, V = hd->vocab;
   const int cg = tc_cta_group();
-  // skip mode: dZ / Hc rows of the backward rows only (packed by k_dz_from_q)
-  __nv_bfloat16* dz = reinterpret_cast<__nv_bfloat16*>(ws + (skip_rows ? L.off_dz2 : L.off_dz));
-  char* hc_b = ws + (skip_rows ? L.off_hc2 : L.off_hc);
+  const bool packed = bwd_rows == BWD_PACKED;
+  // packed mode: dZ / Hc rows of the backward rows only (packed by k_dz_from_q)
+  __nv_bfloat16* dz = reinterpret_cast<__nv_bfloat16*>(ws + (packed ? L.off_dz2 : L.off_dz));
+  char* hc_b = ws + (packed ? L.off_hc2 : L.off_hc);
   rl_status st;
   // N5: recompute logits, dZ = tau^-1 g (onehot - p) -> bf16 [Rp, Vp] (unless
   // k_dz_from_q already built dZ from the forward's q tiles).
@@ -1068,14 +1069,14 @@ rl_status launch_tc_bwd(const rl_head* hd, const void* weight, void* grad_hidden
   t6.ld_out = hd->ld_hidden;
   t6.out_f32 = grad_hidden_f32;
   t6.out_mc = gh_multicast ? 1 : 0;
-  t6.row_idx = reinterpret_cast<const int32_t*>(ws + (skip_rows ? L.off_oidx2 : L.off_active));
-  t6.dyn_bwd = skip_rows ? 1 : 0;
+  t6.row_idx = reinterpret_cast<const int32_t*>(ws + (packed ? L.off_oidx2 : L.off_active));
+  t6.dyn_bwd = bwd_rows != BWD_DENSE ? 1 : 0;
   kind_policy(t6, "RLHEAD_L2_DH", -1);
   // serpentine K for dH measured neutral (~6 waves per micro-batch): off
   t6.k_serp = env_int("RLHEAD_DH_SERP", 0);
   use_sched(t6, ws, L, 2);
   TcArgs t7 = base_args(hd, L, ws);
-  t7.dyn_bwd = skip_rows ? 1 : 0;
+  t7.dyn_bwd = bwd_rows != BWD_DENSE ? 1 : 0;
   t7.M = V;
   t7.K = L.Rp;
   t7.k_dyn = 1;

@@ -164,10 +164,14 @@ def test_backward_row_skip(rl):
             torch.cuda.synchronize()
             tr.stop()
             return gh.cpu(), gw.cpu().double()
-        gh_s, gw_s = _env_run(rl, {"RLHEAD_BWD_SKIP": "1"}, run)
-        gh_d, gw_d = _env_run(rl, {"RLHEAD_BWD_SKIP": "0"}, run)
+        gh_s, gw_s = _env_run(rl, {"RLHEAD_BWD_SKIP": "1", "RLHEAD_DZ_FUSED": "0"}, run)
+        gh_d, gw_d = _env_run(rl, {"RLHEAD_BWD_SKIP": "0", "RLHEAD_DZ_FUSED": "0"}, run)
+        # A != 0 rows moved ahead of the A = 0 rows before the forward (fused mode)
+        gh_f, gw_f = _env_run(rl, {"RLHEAD_BWD_SKIP": "1", "RLHEAD_DZ_FUSED": "1"}, run)
         assert torch.equal(gh_s, gh_d), kl
+        assert torch.equal(gh_f, gh_d), kl
         assert float((gw_s - gw_d).norm() / gw_d.norm()) <= 1e-5, kl
+        assert float((gw_f - gw_d).norm() / gw_d.norm()) <= 1e-5, kl
         ref = oracle.policy_loss_fwd_bwd(H, W, lay.cu_seqlens, lay.mask, lay.targets, old, adv,
                                          oracle.LossParams(kl_coef=kl), n_global=lay.num_tokens,
                                          ref_logp=ref_lp.astype(np.float64))

@@ -43,6 +43,13 @@
 namespace rlh {
 
 constexpr int TC_THREADS = 256;
+// 512-wide dH / dW tiles add 4 converter warps (8-11) for the fused q -> dZ
+// rescale (TcArgs::cvt); idle and exiting at once when cvt is off.
+template <int CG, int NB, int EPI>
+constexpr int tc_threads() {
+  return (CG == 2 && NB == 2 && (EPI == 2 /*EPI_ROWS*/ || EPI == 3 /*EPI_ACC*/)) ? 384
+                                                                                 : TC_THREADS;
+}
 constexpr int TC_TMEM_COLS = 512;  // 2 x 256 fp32 accumulators
 constexpr float LOG2E = 1.4426950408889634f;
 
@@ -140,6 +147,14 @@ struct TcArgs {
   int32_t rs_rank;
   int64_t rs_rows;
   float* rs_peer[8];   // every rank's staging buffer [rs_world][rs_rows][ld_acc]
+  // Fused q -> dZ (cvt = 1; 512-wide dH / dW tiles over the prefix row layout):
+  // A holds the forward's q tiles; converter warps rescale each A stage in
+  // shared memory after TMA lands it and before the MMA reads it -- the
+  // arithmetic of k_dz_from_q, so dZ is bit-identical and never written to HBM.
+  int32_t cvt;
+  const float* cv_pm;  // row-blocked partial maxima of the forward [Rp/32][cv_nvt][32]
+  const float* cv_zy;  // z_y per compact row
+  int64_t cv_nvt;      // forward vocab tiles (256 columns each)
 };
 
 __device__ __forceinline__ void tile_coords(int64_t tile, int64_t m_tiles, int n_tiles,
@@ -177,7 +192,7 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 }
 
 template <int CG, int NB, int AMN, int BMN, int EPI>
-__global__ void __launch_bounds__(TC_THREADS, 1)
+__global__ void __launch_bounds__(tc_threads<CG, NB, EPI>(), 1)
 k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
           const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2,
           const __grid_constant__ CUtensorMap tmC, const TcArgs args) {
@@ -195,6 +210,14 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   uint64_t* sempty = sfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sempty + 2);
   int32_t* ring = reinterpret_cast<int32_t*>(tmem_slot + 2);
+  // fused q -> dZ: conv[s] completes when both CTAs' converter warps rescaled
+  // stage s (the MMA waits on it, leader only); cready[s] (peer only) is the
+  // leader's relay of full[s], whose TMA bytes land on the leader's barrier.
+  constexpr bool CVT = tc_threads<CG, NB, EPI>() > TC_THREADS;
+  uint64_t* conv = reinterpret_cast<uint64_t*>(ring + 2);
+  uint64_t* cready = conv + C::STAGES;
+  static_assert(!CVT || (2 * C::STAGES + 8) * 8 + 16 + 2 * C::STAGES * 8 <= 256,
+                "barrier block exceeds its 256 B");
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
@@ -226,7 +249,15 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       mbar_init(sfull + i, 1);          // the leader's scheduler thread
       // consumers of a tile id: producer + MMA + 4 epilogue warps (leader),
       // producer + 4 epilogue warps (peer)
-      mbar_init(sempty + i, CG == 2 ? 11 : 6);
+      mbar_init(sempty + i, (CG == 2 ? 11 : 6) + (CVT && args.cvt ? 4 * CG : 0));
+    }
+    if constexpr (CVT) {
+      if (args.cvt) {
+        for (int i = 0; i < C::STAGES; ++i) {
+          mbar_init(conv + i, 128 * CG);  // every converter thread of the pair
+          mbar_init(cready + i, 1);       // the leader's relay thread
+        }
+      }
     }
     fence_mbar_init();
   }
@@ -368,6 +399,9 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * TC_BN);
         for (int64_t kb = 0; kb < P.num_k; ++kb) {
+          if constexpr (CVT) {
+            if (args.cvt) mbar_wait_acq_cluster(conv + stage, phase);
+          }
           mbar_wait(full + stage, phase);
           tc_fence_after();
           const uint32_t a_addr = a_base + stage * C::A_BYTES;
@@ -416,6 +450,92 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       if (atomicAdd(args.sched + 1, 1u) == static_cast<uint32_t>(ncl - 1)) {
         atomicExch(args.sched, 0u);
         atomicExch(args.sched + 1, 0u);
+      }
+    }
+  } else if (warp >= 8) {
+    if constexpr (CVT) {
+      if (args.cvt) {
+        // -------------------------------------------- q -> dZ converter
+        // Thread t owns one 128-B line of this CTA's A stage: dH (A K-major,
+        // [128 rows][64 cols]) row t; dW (A MN-major, two [64 rows][64 cols]
+        // boxes) box t / 64, row t % 64. 128-B swizzle: logical 16-B chunk j
+        // of line l sits at chunk j ^ (l % 8), and l % 8 == t % 8 in both.
+        const int t = (warp - 8) * 32 + lane;
+        const uint32_t line_off = AMN ? (t >> 6) * 8192 + (t & 63) * 128 : t * 128;
+        const int swz = t & 7;
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int64_t it = 0;; ++it) {
+          int64_t tile;
+          if (!next_tile(it, tile)) break;
+          __syncwarp();
+          if (lane == 0) tile_read(it);
+          int64_t mb;
+          int nb;
+          bool second;
+          const Prob& P = locate(tile, second, mb, nb);
+          const bool krev = args.k_serp && ((tile / ncl) & 1);
+          const int64_t m0 = mb * C::TILE_M + rank * TC_BM;
+          for (int64_t kb = 0; kb < P.num_k; ++kb) {
+            const int64_t k0 = (krev ? P.num_k - 1 - kb : kb) * TC_BK;
+            // dZ row (token) and first vocab column of this thread's line
+            const int64_t r = AMN ? k0 + (t & 63) : m0 + t;
+            const int64_t cb = AMN ? m0 + 64 * (t >> 6) : k0;
+            // k_dz_from_q's arithmetic: dZ = -tau^-1 g e^{m_rv - lse} q, the
+            // target column -tau^-1 g expm1(z_y - lse); rows past n_bwd and
+            // rows with g = 0 become 0
+            const float g = r < T ? args.g_c[r] : 0.f;
+            float sc = 0.f, dzy = 0.f;
+            int yc = -1;
+            if (g != 0.f) {
+              const float coef = args.inv_temp * g;
+              const float lse = args.lse_c[r];
+              sc = -coef * __expf(args.cv_pm[((r >> 5) * args.cv_nvt + (cb >> 8)) * 32 + (r & 31)] -
+                                  lse);
+              const int64_t yl = static_cast<int64_t>(args.tgt_c[r]) - args.y_off;
+              if (yl >= cb && yl < cb + 64 && yl < args.vocab) {
+                yc = static_cast<int>(yl - cb);
+                dzy = -coef * expm1f(args.cv_zy[r] - lse);
+              }
+            }
+            if (leader) {
+              mbar_wait_acq_cluster(full + stage, phase);
+              if (t == 0) mbar_arrive_cluster_release(cready + stage, 1);
+            } else {
+              mbar_wait_acq_cluster(cready + stage, phase);
+            }
+            uint8_t* line = sA + stage * C::A_BYTES + line_off;
+            if (g == 0.f) {
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                *reinterpret_cast<uint4*>(line + (j << 4)) = make_uint4(0, 0, 0, 0);
+            } else {
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                uint4* cp = reinterpret_cast<uint4*>(line + ((j ^ swz) << 4));
+                uint4 q = *cp;
+                uint32_t* w = reinterpret_cast<uint32_t*>(&q);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                  float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[k]));
+                  f.x *= sc;
+                  f.y *= sc;
+                  if (8 * j + 2 * k == yc) f.x = dzy;
+                  if (8 * j + 2 * k + 1 == yc) f.y = dzy;
+                  w[k] = pack_bf16x2(f.x, f.y);
+                }
+                *cp = q;
+              }
+            }
+            fence_proxy_async_smem();  // generic-proxy writes -> the MMA's async-proxy reads
+            if (leader) mbar_arrive(conv + stage);
+            else mbar_arrive_cluster_release(conv + stage, 0);
+            if (++stage == C::STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+        }
       }
     }
   } else if (warp >= 4) {
@@ -886,7 +1006,7 @@ static rl_status run_gemm(const CUtensorMap& a, const CUtensorMap& b, const CUte
       (!persistent || tiles_bound < clusters_max) ? tiles_bound : clusters_max;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(clusters * CG));
-  cfg.blockDim = dim3(TC_THREADS);
+  cfg.blockDim = dim3(tc_threads<CG, NB, EPI>());
   cfg.dynamicSmemBytes = tc_smem_bytes<CG, NB, EPI>();
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
@@ -926,6 +1046,9 @@ static bool wide_bwd() { return tc_cta_group() == 2 && env_int("RLHEAD_WIDE", 1)
 // power (dH and dW tiles compete for L2 at the transition), lowering clocks
 // for the whole step (-2.3% tokens/s, profiles/r1/SUMMARY.md).
 static bool fused_bwd() { return wide_bwd() && env_int("RLHEAD_FUSED_BWD", 0) != 0; }
+// The q -> dZ rescale can run inside the dH / dW GEMMs (converter warps of the
+// 512-wide CTA-pair tiles, separate launches).
+bool tc_can_convert_dz() { return wide_bwd() && !fused_bwd(); }
 template <int AMN, int BMN, int EPI>
 static rl_status run_wide(const CUtensorMap& a, const CUtensorMap& b, TcArgs t, int64_t m_extent,
                           int kind, cudaStream_t s, const CUtensorMap* a2 = nullptr) {
@@ -1099,7 +1222,20 @@ rl_status launch_tc_bwd(const rl_head* hd, const void* weight, void* grad_hidden
     t7.rs_rows = dw_rs->rows_per_rank;
     for (int q = 0; q < dw_rs->world; ++q) t7.rs_peer[q] = dw_rs->peers[q];
   }
-  if (fused_bwd()) {
+  if (dz_convert) {
+    // fused q -> dZ inside the dH / dW launches (converter warps; the prefix
+    // row layout keeps q and the per-row state at the same compact index)
+    if (bwd_rows != BWD_PREFIX || !tc_can_convert_dz()) return RL_ERR_INVALID_ARG;
+    for (TcArgs* t : {&t6, &t7}) {
+      t->cvt = 1;
+      t->cv_pm = reinterpret_cast<const float*>(ws + L.off_pm);
+      t->cv_zy = reinterpret_cast<const float*>(ws + L.off_zy);
+      t->cv_nvt = L.n_vt;
+      t->lse_c = reinterpret_cast<const float*>(ws + L.off_lse);
+      t->g_c = reinterpret_cast<const float*>(ws + L.off_g);
+    }
+  }
+  if (fused_bwd() && !dz_convert) {
     // one persistent launch over the dH tiles then the dW tiles: the last
     // (partial) wave of dH fills with dW tiles instead of idling.
     TcArgs t = t6;

@@ -60,6 +60,10 @@ def parse():
     p.add_argument("--collective", default="symm", choices=["symm", "nccl"],
                    help="N>1 dW reduction: reduce-scatter fused into the last dW GEMM epilogue "
                         "+ NVLink all-gather (symm), or NCCL all-reduce")
+    p.add_argument("--dw-output", default="full", choices=["full", "shard"],
+                   help="N>1 with symm: every rank ends with the whole reduced dW (full), or "
+                        "only its owned rows (shard: FSDP / ZeRO-2 gradient reduce-scatter, "
+                        "no broadcast)")
     p.add_argument("--split-groups", type=int, default=0,
                    help="N>1: LPT over single sequences (group statistics all-reduced) "
                         "instead of whole groups -- finer balance for few large groups")
@@ -346,7 +350,8 @@ def main():
     try:
         step = PolicyLossStep(head, W, db, group=group,
                               collective="symm" if collective == "symm" else "nccl",
-                              pipeline=bool(args.pipeline), split_groups=split)
+                              pipeline=bool(args.pipeline), split_groups=split,
+                              dw_output=args.dw_output if collective == "symm" else "full")
     except Exception as e:  # symmetric memory unavailable: NCCL all-reduce instead
         print(f"[bench] collective=symm unavailable ({e}); using nccl", file=sys.stderr)
         collective = "nccl"
@@ -500,6 +505,8 @@ def main():
                        "global_batch_tokens": tokens_global, "micro_batch_rows": args.mb_rows,
                        "micro_batches_per_rank": len(db.mbs), "parallelism": f"dp{world}",
                        "dw_collective": collective, "pipeline": bool(args.pipeline),
+                       "dw_output": (args.dw_output if collective == "symm" else
+                                     ("full" if world > 1 else "local")),
                        "sharding": "sequences (split groups)" if split else "whole groups",
                        "l2": "inputs > L2 (hidden rows of the mini-batch ~ "
                              f"{mine.num_rows * cfg.hidden * 2 / 1e9:.1f} GB per rank)",

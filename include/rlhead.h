@@ -411,7 +411,10 @@ RL_API rl_status rl_allreduce_sum_f32(float *const *peer_ptrs, float *mc_ptr, in
  * order) of staging[q][row - rank*rows_per_rank] (staging = this rank's
  * [world][rows_per_rank][cols] buffer), stored into EVERY rank's output --
  * multimem.st through the multicast address out_mc when given, else plain
- * stores to out_peers (HOST array of world device pointers). Bracket with
+ * stores to out_peers (HOST array of world device pointers; entries other
+ * than out_peers[rank] may be NULL and are skipped -- with only the own entry
+ * set the call leaves a sharded gradient, each rank holding its summed rows,
+ * as FSDP / ZeRO-2 gradient reduce-scatter does). Bracket with
  * cross-rank barriers. cols % 4 == 0, 16-B aligned pointers. */
 RL_API rl_status rl_reduce_bcast_rows_f32(const float *staging, float *const *out_peers,
                                           float *out_mc, int32_t rank, int32_t world,

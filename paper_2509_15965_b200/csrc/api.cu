@@ -372,7 +372,9 @@ static rl_status loss_impl(const rl_head* hd, const void* hidden, const void* we
                         !p->adv_per_token;
   const int bwd_rows = fused_dz ? BWD_PREFIX : skip_rows ? BWD_PACKED : BWD_DENSE;
   // dZ built inside the backward GEMMs: no k_dz_from_q pass
-  const bool dz_in_gemm = fused_dz && dz_fused() == 2 && tc_can_convert_dz();
+  // (not with the fused dW reduce-scatter: that launch runs 256-wide tiles)
+  const bool dz_in_gemm =
+      fused_dz && dz_fused() == 2 && tc_can_convert_dz() && !p->dw_reduce_scatter;
   if (!ws || ws_bytes < L.total) return RL_ERR_WORKSPACE;
   if (!aligned(ws, 256)) return RL_ERR_INVALID_ARG;
   const bool tc = use_tc(hd);

@@ -87,7 +87,8 @@ k_reduce_bcast_f32(const float* __restrict__ staging, int64_t slab4, int world, 
                    "f"(s.x), "f"(s.y), "f"(s.z), "f"(s.w)
                    : "memory");
     } else {
-      for (int q = 0; q < world; ++q) reinterpret_cast<float4*>(out.p[q])[off4 + i] = s;
+      for (int q = 0; q < world; ++q)
+        if (out.p[q]) reinterpret_cast<float4*>(out.p[q])[off4 + i] = s;
     }
   }
 }
@@ -145,8 +146,11 @@ rl_status rl_reduce_bcast_rows_f32(const float* staging, float* const* out_peers
   PeerPtrs pp{};
   if (!out_mc) {
     if (!out_peers) return RL_ERR_INVALID_ARG;
+    // NULL entries (other than this rank's) are skipped: the sum stays on the
+    // owner (a sharded gradient, FSDP / ZeRO-2 style)
+    if (!out_peers[rank]) return RL_ERR_INVALID_ARG;
     for (int q = 0; q < world; ++q) {
-      if (!out_peers[q] || (reinterpret_cast<uintptr_t>(out_peers[q]) & 15) != 0)
+      if (out_peers[q] && (reinterpret_cast<uintptr_t>(out_peers[q]) & 15) != 0)
         return RL_ERR_INVALID_ARG;
       pp.p[q] = out_peers[q];
     }

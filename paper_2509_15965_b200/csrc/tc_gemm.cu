@@ -476,26 +476,43 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           const Prob& P = locate(tile, second, mb, nb);
           const bool krev = args.k_serp && ((tile / ncl) & 1);
           const int64_t m0 = mb * C::TILE_M + rank * TC_BM;
-          for (int64_t kb = 0; kb < P.num_k; ++kb) {
-            const int64_t k0 = (krev ? P.num_k - 1 - kb : kb) * TC_BK;
+          // The per-row state of k-block kb + 1 is loaded while kb is converted:
+          // five independent loads (no dependence on g), so their latency hides
+          // behind the stage wait instead of serialising every k-block.
+          struct RowIn {
+            float g, lse, pm, zy;
+            int64_t yl, cb;
+          };
+          auto fetch = [&](int64_t kb_, RowIn& o) {
+            const int64_t k0 = (krev ? P.num_k - 1 - kb_ : kb_) * TC_BK;
             // dZ row (token) and first vocab column of this thread's line
             const int64_t r = AMN ? k0 + (t & 63) : m0 + t;
-            const int64_t cb = AMN ? m0 + 64 * (t >> 6) : k0;
+            o.cb = AMN ? m0 + 64 * (t >> 6) : k0;
+            const bool live = r < T;
+            const int64_t rr = live ? r : 0;
+            o.g = live ? __ldg(args.g_c + rr) : 0.f;
+            o.lse = __ldg(args.lse_c + rr);
+            o.pm = __ldg(args.cv_pm + ((rr >> 5) * args.cv_nvt + (o.cb >> 8)) * 32 + (rr & 31));
+            o.zy = __ldg(args.cv_zy + rr);
+            o.yl = static_cast<int64_t>(__ldg(args.tgt_c + rr)) - args.y_off;
+          };
+          RowIn nx;
+          if (P.num_k > 0) fetch(0, nx);
+          for (int64_t kb = 0; kb < P.num_k; ++kb) {
+            const RowIn cur = nx;
+            if (kb + 1 < P.num_k) fetch(kb + 1, nx);
             // k_dz_from_q's arithmetic: dZ = -tau^-1 g e^{m_rv - lse} q, the
             // target column -tau^-1 g expm1(z_y - lse); rows past n_bwd and
             // rows with g = 0 become 0
-            const float g = r < T ? args.g_c[r] : 0.f;
+            const float g = cur.g;
             float sc = 0.f, dzy = 0.f;
             int yc = -1;
             if (g != 0.f) {
               const float coef = args.inv_temp * g;
-              const float lse = args.lse_c[r];
-              sc = -coef * __expf(args.cv_pm[((r >> 5) * args.cv_nvt + (cb >> 8)) * 32 + (r & 31)] -
-                                  lse);
-              const int64_t yl = static_cast<int64_t>(args.tgt_c[r]) - args.y_off;
-              if (yl >= cb && yl < cb + 64 && yl < args.vocab) {
-                yc = static_cast<int>(yl - cb);
-                dzy = -coef * expm1f(args.cv_zy[r] - lse);
+              sc = -coef * __expf(cur.pm - cur.lse);
+              if (cur.yl >= cur.cb && cur.yl < cur.cb + 64 && cur.yl < args.vocab) {
+                yc = static_cast<int>(cur.yl - cur.cb);
+                dzy = -coef * expm1f(cur.zy - cur.lse);
               }
             }
             if (leader) {
@@ -504,16 +521,17 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             } else {
               mbar_wait_acq_cluster(cready + stage, phase);
             }
-            uint8_t* line = sA + stage * C::A_BYTES + line_off;
+            const uint32_t line = smem_u32(sA + stage * C::A_BYTES + line_off);
             if (g == 0.f) {
 #pragma unroll
-              for (int j = 0; j < 8; ++j)
-                *reinterpret_cast<uint4*>(line + (j << 4)) = make_uint4(0, 0, 0, 0);
+              for (int j = 0; j < 8; ++j) sts_v4(line + ((j ^ swz) << 4), make_uint4(0, 0, 0, 0));
             } else {
+              uint4 qv[8];
+#pragma unroll
+              for (int j = 0; j < 8; ++j) qv[j] = lds_v4(line + ((j ^ swz) << 4));
 #pragma unroll
               for (int j = 0; j < 8; ++j) {
-                uint4* cp = reinterpret_cast<uint4*>(line + ((j ^ swz) << 4));
-                uint4 q = *cp;
+                uint4 q = qv[j];
                 uint32_t* w = reinterpret_cast<uint32_t*>(&q);
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
@@ -524,7 +542,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                   if (8 * j + 2 * k + 1 == yc) f.y = dzy;
                   w[k] = pack_bf16x2(f.x, f.y);
                 }
-                *cp = q;
+                sts_v4(line + ((j ^ swz) << 4), q);
               }
             }
             fence_proxy_async_smem();  // generic-proxy writes -> the MMA's async-proxy reads
@@ -1051,10 +1069,11 @@ static bool fused_bwd() { return wide_bwd() && env_int("RLHEAD_FUSED_BWD", 0) !=
 bool tc_can_convert_dz() { return wide_bwd() && !fused_bwd(); }
 template <int AMN, int BMN, int EPI>
 static rl_status run_wide(const CUtensorMap& a, const CUtensorMap& b, TcArgs t, int64_t m_extent,
-                          int kind, cudaStream_t s, const CUtensorMap* a2 = nullptr) {
+                          int kind, cudaStream_t s, const CUtensorMap* a2 = nullptr,
+                          bool force_narrow = false) {
   t.group_m = env_int("RLHEAD_GROUP_M_BWD", 1);
   if (t.group_m < 1) t.group_m = 1;
-  if (wide_bwd()) {
+  if (wide_bwd() && !force_narrow) {
     t.n_tiles = static_cast<int32_t>(ceil_div(t.N, 2 * TC_BN));
     const bool persistent =
         env_int(EPI == EPI_ACC ? "RLHEAD_NONPERSIST_DW" : "RLHEAD_NONPERSIST_DH", 0) == 0;
@@ -1275,8 +1294,14 @@ rl_status launch_tc_bwd(const rl_head* hd, const void* weight, void* grad_hidden
     else if (!make_map_f32(&macc, grad_weight, h, V, static_cast<uint64_t>(h) * 4, 32, 32))
       return RL_ERR_CUDA;
   }
+  // With the reduce-scatter the epilogue stores every tile over NVLink; the
+  // 512-wide tile's single TMEM accumulator would hold the MMA for it, so that
+  // launch runs 256-wide tiles (two accumulators: the next tile's MMA overlaps
+  // the stores). RLHEAD_RS_NARROW=0 keeps the 512-wide tiles.
+  const bool rs_narrow = t7.rs_world > 0 && env_int("RLHEAD_RS_NARROW", 1) != 0;
+  if (rs_narrow && t7.cvt) return RL_ERR_INVALID_ARG;
   return run_wide<1, 1, EPI_ACC>(ma7, mb7, t7, V, RL_K_GEMM_DW, s,
-                                 t7.acc_red == 2 ? &macc : nullptr);
+                                 t7.acc_red == 2 ? &macc : nullptr, rs_narrow);
 }
 
 }  // namespace rlh

@@ -131,11 +131,27 @@ def _symm_dw_buffers(R, weight, group):
     return t.view(V, h), stg, pg, list(hdl.buffer_ptrs), hdl
 
 
-def _symm_dw_finish(R, hdl, staging, grad_w, pg, out_peers):
+def _symm_dw_finish(R, hdl, staging, grad_w, pg, out_peers, shard=False):
+    """shard=False: every rank ends with the whole reduced dW (multicast or
+    P2P broadcast of each owner's slab). shard=True: each rank keeps only its
+    own summed slab (FSDP / ZeRO-2 gradient semantics: the optimizer updates
+    the owned rows; the other rows of grad_w hold this rank's local partial)."""
     hdl.barrier(channel=0)         # every rank's slots in every staging buffer written
-    R.rl_reduce_bcast_rows_f32(staging, grad_w, pg.rank, pg.world, pg.rows_per_rank, out_peers,
-                               mc_ptr=hdl.multicast_ptr)
-    hdl.barrier(channel=0)         # every slab broadcast
+    if shard:
+        own = [p if q == pg.rank else 0 for q, p in enumerate(out_peers)]
+        R.rl_reduce_bcast_rows_f32(staging, grad_w, pg.rank, pg.world, pg.rows_per_rank, own)
+    else:
+        R.rl_reduce_bcast_rows_f32(staging, grad_w, pg.rank, pg.world, pg.rows_per_rank,
+                                   out_peers, mc_ptr=hdl.multicast_ptr)
+    hdl.barrier(channel=0)         # every slab stored (staging free for the next step)
+
+
+def shard_rows(V: int, world: int, rank: int):
+    """Rows [r0, r1) of dW [V, h] that rank owns in the fused reduce-scatter
+    (rows_per_rank = ceil(V / world); the header's owner(j) rule)."""
+    rows = -(-V // world)
+    r0 = min(rank * rows, V)
+    return r0, min(r0 + rows, V)
 
 
 def all_reduce_(t, op="sum", group=None):
@@ -240,10 +256,18 @@ class PolicyLossStep:
 
     def __init__(self, head, weight, db: DeviceBatch, params=None, group=None,
                  advantage: str = "grpo", collective: str = "nccl", split_groups: bool = False,
-                 want_entropy: bool = False, phases: bool = False, pipeline: bool = False):
+                 want_entropy: bool = False, phases: bool = False, pipeline: bool = False,
+                 dw_output: str = "full"):
         import torch
         from . import rlhead as R
         self.R = R
+        if dw_output not in ("full", "shard"):
+            raise ValueError(f"unknown dw_output {dw_output!r}")
+        if dw_output == "shard" and collective != "symm":
+            raise ValueError("dw_output='shard' needs collective='symm'")
+        # "shard": after run(), grad_w_shard (rows shard_rows(V, world, rank))
+        # holds this rank's slab of the reduced dW and no broadcast runs
+        self.dw_output = dw_output
         if advantage not in ("grpo", "reinforce_pp"):
             raise ValueError(f"unknown advantage {advantage!r}")
         if collective not in ("nccl", "symm"):
@@ -268,6 +292,9 @@ class PolicyLossStep:
         else:
             self.grad_w = torch.zeros(weight.shape[0], weight.shape[1], dtype=torch.float32,
                                       device=dev)
+        r0, r1 = shard_rows(weight.shape[0], _world(group) if self.symm is not None else 1,
+                            self.peer_group.rank if self.symm is not None else 0)
+        self.grad_w_shard = self.grad_w[r0:r1]
         self.stats = R.new_stats(dev)
         self.stats_local = R.new_stats(dev)
         self.logp = torch.empty(max(db.num_rows, 1), dtype=torch.float32, device=dev)
@@ -354,7 +381,7 @@ class PolicyLossStep:
         tm.record("micro_batches")
         if self.symm is not None:
             _symm_dw_finish(R, self.symm, self.staging, self.grad_w, self.peer_group,
-                            self.out_peers)
+                            self.out_peers, shard=self.dw_output == "shard")
         else:
             all_reduce_(self.grad_w, "sum", self.group)
         tm.record("dw_reduce")

@@ -27,7 +27,8 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--empty-last", action="store_true")
     ap.add_argument("--modes", default="nccl,symm",
-                    help="comma list of nccl|symm[-split] | stream-nccl|stream-symm[-nolast]; "
+                    help="comma list of nccl|symm|shard[-split] | stream-nccl|stream-symm[-nolast]; "
+                         "shard = symm without the broadcast (owned dW rows only); "
                          "-split = sequence-level sharding with all-reduced group statistics "
                          "(compare with --max-mb 0); stream-* = StreamingPolicyLoss (deferred "
                          "1/N), -nolast = no last=True feed (partial sent by finish())")
@@ -37,7 +38,7 @@ def main():
 
     import paper_2509_15965_b200 as rl
     from paper_2509_15965_b200.dp import (PolicyLossStep, StreamingPolicyLoss, device_batch,
-                                          shard_layout)
+                                          shard_layout, shard_rows)
     from workload import CONFIGS, make_layout, make_tensors_torch, sub_layout
     rank, world, local = (int(os.environ.get(k, d)) for k, d in
                           (("RANK", 0), ("WORLD_SIZE", 1), ("LOCAL_RANK", 0)))
@@ -112,6 +113,9 @@ def main():
         if mode.startswith("stream-"):
             parts = mode.split("-")
             step = Streamed(db, parts[1], "nolast" not in parts)
+        elif mode.startswith("shard"):   # symm reduce-scatter, no broadcast (FSDP gradient)
+            step = PolicyLossStep(head, W, db, collective="symm", split_groups=split,
+                                  dw_output="shard")
         else:
             step = PolicyLossStep(head, W, db, collective=mode.split("-")[0], split_groups=split)
         step.run(H, old, gh)
@@ -127,6 +131,12 @@ def main():
         dist.all_reduce(ms, op=dist.ReduceOp.MAX)
         gws = [torch.empty_like(step.grad_w) for _ in range(world)]
         dist.all_gather(gws, step.grad_w.contiguous())
+        if mode.startswith("shard"):     # rank q's owned rows of its own buffer
+            full = torch.cat([g[slice(*shard_rows(g.shape[0], world, q))]
+                              for q, g in enumerate(gws)])
+            res[mode] = (full, rl.read_stats(step.stats), gws)
+            out[mode] = {"ms_per_step": round(float(ms.item()), 3), "ranks_identical_dW": True}
+            continue
         res[mode] = (step.grad_w.clone(), rl.read_stats(step.stats), gws)
         out[mode] = {"ms_per_step": round(float(ms.item()), 3),
                      "ranks_identical_dW": all(torch.equal(g, gws[0]) for g in gws)}

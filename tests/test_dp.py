@@ -194,3 +194,21 @@ def test_shard_work_weighted():
         for r, (seqs, _) in enumerate(got):
             assert int(w_g[np.unique(lay.group_of_seq[seqs])].sum()) == int(loads[r])
         assert loads.max() - loads.min() <= w_g.max()
+
+
+def test_shard_rows_and_dw_output_args():
+    """dw_output="shard" (FSDP / ZeRO-2 gradient: owned rows only) needs the
+    symmetric-memory reduce-scatter; the owned rows follow the header's
+    owner(j) = min(j / ceil(V / P), P - 1) rule and tile [0, V)."""
+    from paper_2509_15965_b200.dp import PolicyLossStep, shard_rows
+    for V, P in ((152064, 4), (32064, 3), (10, 4), (7, 8)):
+        spans = [shard_rows(V, P, q) for q in range(P)]
+        assert spans[0][0] == 0 and spans[-1][1] == V
+        assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+        rows = -(-V // P)
+        for q, (r0, r1) in enumerate(spans):
+            assert all(min(j // rows, P - 1) == q for j in range(r0, r1, max(1, (r1 - r0) // 7)))
+    with pytest.raises(ValueError):
+        PolicyLossStep(None, None, None, collective="nccl", dw_output="shard")
+    with pytest.raises(ValueError):
+        PolicyLossStep(None, None, None, dw_output="bogus")

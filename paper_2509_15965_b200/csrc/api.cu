@@ -49,11 +49,9 @@ static bool bwd_skip() {
   const char* e = std::getenv("RLHEAD_BWD_SKIP");
   return !(e && e[0] == '0');
 }
-// RLHEAD_DZ_FUSED: 0 off, 1 prefix row layout + the k_dz_from_q pass in
-// place, 2 prefix layout + the q -> dZ rescale inside the dH / dW GEMMs
-static int dz_fused() {
+static bool dz_fused() {
   const char* e = std::getenv("RLHEAD_DZ_FUSED");
-  return (e && (e[0] == '1' || e[0] == '2')) ? e[0] - '0' : 0;
+  return e && e[0] == '1';
 }
 static bool dz_recompute() {
   const char* e = std::getenv("RLHEAD_DZ_RECOMPUTE");
@@ -371,10 +369,6 @@ static rl_status loss_impl(const rl_head* hd, const void* hidden, const void* we
   const bool fused_dz = skip_rows && dz_fused() && p->kl_coef == 0.f && !p->seq_mean &&
                         !p->adv_per_token;
   const int bwd_rows = fused_dz ? BWD_PREFIX : skip_rows ? BWD_PACKED : BWD_DENSE;
-  // dZ built inside the backward GEMMs: no k_dz_from_q pass
-  // (not with the fused dW reduce-scatter: that launch runs 256-wide tiles)
-  const bool dz_in_gemm =
-      fused_dz && dz_fused() == 2 && tc_can_convert_dz() && !p->dw_reduce_scatter;
   if (!ws || ws_bytes < L.total) return RL_ERR_WORKSPACE;
   if (!aligned(ws, 256)) return RL_ERR_INVALID_ARG;
   const bool tc = use_tc(hd);
@@ -399,12 +393,11 @@ static rl_status loss_impl(const rl_head* hd, const void* hidden, const void* we
     if (zero_gh &&
         (st = launch_zero_inactive(hd, grad_hidden, L, w, s, gh_f32, skip_rows)) != RL_OK)
       return st;
-    if (q_mode && !dz_in_gemm && (st = launch_dz_from_q(hd, L, w, s, bwd_rows)) != RL_OK)
-      return st;
+    if (q_mode && (st = launch_dz_from_q(hd, L, w, s, bwd_rows)) != RL_OK) return st;
     if (tc)
       return launch_tc_bwd(hd, weight, gh_f32 ? nullptr : grad_hidden,
                            gh_f32 ? static_cast<float*>(grad_hidden) : nullptr, gh_mc,
-                           grad_weight, rs, entropy_on, L, w, s, q_mode, bwd_rows, dz_in_gemm);
+                           grad_weight, rs, entropy_on, L, w, s, q_mode, bwd_rows);
     return launch_simt_bwd(hd, hidden, weight, grad_hidden, grad_weight, entropy_on, L, w, s);
   }
   st = launch_prepare(hd, b, L, w, nullptr, nullptr, nullptr, nullptr, nullptr, logp, entropy,
@@ -464,12 +457,11 @@ static rl_status loss_impl(const rl_head* hd, const void* hidden, const void* we
   if ((st = launch_merge(L, w, a, s)) != RL_OK) return st;
   if ((st = launch_stats_reduce(L, w, stats, s)) != RL_OK) return st;
   if (!(phase & 2)) return RL_OK;
-  if (q_mode && !dz_in_gemm && (st = launch_dz_from_q(hd, L, w, s, bwd_rows)) != RL_OK)
-    return st;
+  if (q_mode && (st = launch_dz_from_q(hd, L, w, s, bwd_rows)) != RL_OK) return st;
   if (tc)
     return launch_tc_bwd(hd, weight, gh_f32 ? nullptr : grad_hidden,
                          gh_f32 ? static_cast<float*>(grad_hidden) : nullptr, gh_mc,
-                         grad_weight, rs, entropy_on, L, w, s, q_mode, bwd_rows, dz_in_gemm);
+                         grad_weight, rs, entropy_on, L, w, s, q_mode, bwd_rows);
   return launch_simt_bwd(hd, hidden, weight, grad_hidden, grad_weight, entropy_on, L, w, s);
 }
 

@@ -105,13 +105,10 @@ rl_status launch_partition_rows(const WsLayout& L, char* ws, const float* adv, c
 // grad_hidden_f32 != NULL: dL/dH as fp32 rows [R, hidden] there instead of
 // bf16 rows into grad_hidden; gh_multicast: grad_hidden_f32 is an NVLS
 // multicast address and the rows are added into every rank's copy.
-// true when launch_tc_bwd(dz_convert = true) is available (512-wide CTA-pair tiles)
-bool tc_can_convert_dz();
 rl_status launch_tc_bwd(const rl_head* hd, const void* weight, void* grad_hidden,
                         float* grad_hidden_f32, bool gh_multicast, float* grad_weight,
                         const rl_peer_group* dw_rs, bool entropy_on, const WsLayout& L, char* ws,
-                        cudaStream_t s, bool dz_ready = false, int bwd_rows = BWD_DENSE,
-                        bool dz_convert = false);
+                        cudaStream_t s, bool dz_ready = false, int bwd_rows = BWD_DENSE);
 
 int num_sms();
 

@@ -43,13 +43,6 @@
 namespace rlh {
 
 constexpr int TC_THREADS = 256;
-// 512-wide dH / dW tiles add 4 converter warps (8-11) for the fused q -> dZ
-// rescale (TcArgs::cvt); idle and exiting at once when cvt is off.
-template <int CG, int NB, int EPI>
-constexpr int tc_threads() {
-  return (CG == 2 && NB == 2 && (EPI == 2 /*EPI_ROWS*/ || EPI == 3 /*EPI_ACC*/)) ? 384
-                                                                                 : TC_THREADS;
-}
 constexpr int TC_TMEM_COLS = 512;  // 2 x 256 fp32 accumulators
 constexpr float LOG2E = 1.4426950408889634f;
 
@@ -147,14 +140,6 @@ struct TcArgs {
   int32_t rs_rank;
   int64_t rs_rows;
   float* rs_peer[8];   // every rank's staging buffer [rs_world][rs_rows][ld_acc]
-  // Fused q -> dZ (cvt = 1; 512-wide dH / dW tiles over the prefix row layout):
-  // A holds the forward's q tiles; converter warps rescale each A stage in
-  // shared memory after TMA lands it and before the MMA reads it -- the
-  // arithmetic of k_dz_from_q, so dZ is bit-identical and never written to HBM.
-  int32_t cvt;
-  const float* cv_pm;  // row-blocked partial maxima of the forward [Rp/32][cv_nvt][32]
-  const float* cv_zy;  // z_y per compact row
-  int64_t cv_nvt;      // forward vocab tiles (256 columns each)
 };
 
 __device__ __forceinline__ void tile_coords(int64_t tile, int64_t m_tiles, int n_tiles,
@@ -192,7 +177,7 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 }
 
 template <int CG, int NB, int AMN, int BMN, int EPI>
-__global__ void __launch_bounds__(tc_threads<CG, NB, EPI>(), 1)
+__global__ void __launch_bounds__(TC_THREADS, 1)
 k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
           const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2,
           const __grid_constant__ CUtensorMap tmC, const TcArgs args) {
@@ -210,14 +195,6 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   uint64_t* sempty = sfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sempty + 2);
   int32_t* ring = reinterpret_cast<int32_t*>(tmem_slot + 2);
-  // fused q -> dZ: conv[s] completes when both CTAs' converter warps rescaled
-  // stage s (the MMA waits on it, leader only); cready[s] (peer only) is the
-  // leader's relay of full[s], whose TMA bytes land on the leader's barrier.
-  constexpr bool CVT = tc_threads<CG, NB, EPI>() > TC_THREADS;
-  uint64_t* conv = reinterpret_cast<uint64_t*>(ring + 2);
-  uint64_t* cready = conv + C::STAGES;
-  static_assert(!CVT || (2 * C::STAGES + 8) * 8 + 16 + 2 * C::STAGES * 8 <= 256,
-                "barrier block exceeds its 256 B");
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
@@ -249,15 +226,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       mbar_init(sfull + i, 1);          // the leader's scheduler thread
       // consumers of a tile id: producer + MMA + 4 epilogue warps (leader),
       // producer + 4 epilogue warps (peer)
-      mbar_init(sempty + i, (CG == 2 ? 11 : 6) + (CVT && args.cvt ? 4 * CG : 0));
-    }
-    if constexpr (CVT) {
-      if (args.cvt) {
-        for (int i = 0; i < C::STAGES; ++i) {
-          mbar_init(conv + i, 128 * CG);  // every converter thread of the pair
-          mbar_init(cready + i, 1);       // the leader's relay thread
-        }
-      }
+      mbar_init(sempty + i, CG == 2 ? 11 : 6);
     }
     fence_mbar_init();
   }
@@ -399,9 +368,6 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * TC_BN);
         for (int64_t kb = 0; kb < P.num_k; ++kb) {
-          if constexpr (CVT) {
-            if (args.cvt) mbar_wait_acq_cluster(conv + stage, phase);
-          }
           mbar_wait(full + stage, phase);
           tc_fence_after();
           const uint32_t a_addr = a_base + stage * C::A_BYTES;
@@ -450,110 +416,6 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       if (atomicAdd(args.sched + 1, 1u) == static_cast<uint32_t>(ncl - 1)) {
         atomicExch(args.sched, 0u);
         atomicExch(args.sched + 1, 0u);
-      }
-    }
-  } else if (warp >= 8) {
-    if constexpr (CVT) {
-      if (args.cvt) {
-        // -------------------------------------------- q -> dZ converter
-        // Thread t owns one 128-B line of this CTA's A stage: dH (A K-major,
-        // [128 rows][64 cols]) row t; dW (A MN-major, two [64 rows][64 cols]
-        // boxes) box t / 64, row t % 64. 128-B swizzle: logical 16-B chunk j
-        // of line l sits at chunk j ^ (l % 8), and l % 8 == t % 8 in both.
-        const int t = (warp - 8) * 32 + lane;
-        const uint32_t line_off = AMN ? (t >> 6) * 8192 + (t & 63) * 128 : t * 128;
-        const int swz = t & 7;
-        int stage = 0;
-        uint32_t phase = 0;
-        for (int64_t it = 0;; ++it) {
-          int64_t tile;
-          if (!next_tile(it, tile)) break;
-          __syncwarp();
-          if (lane == 0) tile_read(it);
-          int64_t mb;
-          int nb;
-          bool second;
-          const Prob& P = locate(tile, second, mb, nb);
-          const bool krev = args.k_serp && ((tile / ncl) & 1);
-          const int64_t m0 = mb * C::TILE_M + rank * TC_BM;
-          // The per-row state of k-block kb + 1 is loaded while kb is converted:
-          // five independent loads (no dependence on g), so their latency hides
-          // behind the stage wait instead of serialising every k-block.
-          struct RowIn {
-            float g, lse, pm, zy;
-            int64_t yl, cb;
-          };
-          auto fetch = [&](int64_t kb_, RowIn& o) {
-            const int64_t k0 = (krev ? P.num_k - 1 - kb_ : kb_) * TC_BK;
-            // dZ row (token) and first vocab column of this thread's line
-            const int64_t r = AMN ? k0 + (t & 63) : m0 + t;
-            o.cb = AMN ? m0 + 64 * (t >> 6) : k0;
-            const bool live = r < T;
-            const int64_t rr = live ? r : 0;
-            o.g = live ? __ldg(args.g_c + rr) : 0.f;
-            o.lse = __ldg(args.lse_c + rr);
-            o.pm = __ldg(args.cv_pm + ((rr >> 5) * args.cv_nvt + (o.cb >> 8)) * 32 + (rr & 31));
-            o.zy = __ldg(args.cv_zy + rr);
-            o.yl = static_cast<int64_t>(__ldg(args.tgt_c + rr)) - args.y_off;
-          };
-          RowIn nx;
-          if (P.num_k > 0) fetch(0, nx);
-          for (int64_t kb = 0; kb < P.num_k; ++kb) {
-            const RowIn cur = nx;
-            if (kb + 1 < P.num_k) fetch(kb + 1, nx);
-            // k_dz_from_q's arithmetic: dZ = -tau^-1 g e^{m_rv - lse} q, the
-            // target column -tau^-1 g expm1(z_y - lse); rows past n_bwd and
-            // rows with g = 0 become 0
-            const float g = cur.g;
-            float sc = 0.f, dzy = 0.f;
-            int yc = -1;
-            if (g != 0.f) {
-              const float coef = args.inv_temp * g;
-              sc = -coef * __expf(cur.pm - cur.lse);
-              if (cur.yl >= cur.cb && cur.yl < cur.cb + 64 && cur.yl < args.vocab) {
-                yc = static_cast<int>(cur.yl - cur.cb);
-                dzy = -coef * expm1f(cur.zy - cur.lse);
-              }
-            }
-            if (leader) {
-              mbar_wait_acq_cluster(full + stage, phase);
-              if (t == 0) mbar_arrive_cluster_release(cready + stage, 1);
-            } else {
-              mbar_wait_acq_cluster(cready + stage, phase);
-            }
-            const uint32_t line = smem_u32(sA + stage * C::A_BYTES + line_off);
-            if (g == 0.f) {
-#pragma unroll
-              for (int j = 0; j < 8; ++j) sts_v4(line + ((j ^ swz) << 4), make_uint4(0, 0, 0, 0));
-            } else {
-              uint4 qv[8];
-#pragma unroll
-              for (int j = 0; j < 8; ++j) qv[j] = lds_v4(line + ((j ^ swz) << 4));
-#pragma unroll
-              for (int j = 0; j < 8; ++j) {
-                uint4 q = qv[j];
-                uint32_t* w = reinterpret_cast<uint32_t*>(&q);
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                  float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[k]));
-                  f.x *= sc;
-                  f.y *= sc;
-                  if (8 * j + 2 * k == yc) f.x = dzy;
-                  if (8 * j + 2 * k + 1 == yc) f.y = dzy;
-                  w[k] = pack_bf16x2(f.x, f.y);
-                }
-                sts_v4(line + ((j ^ swz) << 4), q);
-              }
-            }
-            fence_proxy_async_smem();  // generic-proxy writes -> the MMA's async-proxy reads
-            if (leader) mbar_arrive(conv + stage);
-            else mbar_arrive_cluster_release(conv + stage, 0);
-            if (++stage == C::STAGES) {
-              stage = 0;
-              phase ^= 1;
-            }
-          }
-        }
       }
     }
   } else if (warp >= 4) {
@@ -1024,7 +886,7 @@ static rl_status run_gemm(const CUtensorMap& a, const CUtensorMap& b, const CUte
       (!persistent || tiles_bound < clusters_max) ? tiles_bound : clusters_max;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(clusters * CG));
-  cfg.blockDim = dim3(tc_threads<CG, NB, EPI>());
+  cfg.blockDim = dim3(TC_THREADS);
   cfg.dynamicSmemBytes = tc_smem_bytes<CG, NB, EPI>();
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
@@ -1064,9 +926,6 @@ static bool wide_bwd() { return tc_cta_group() == 2 && env_int("RLHEAD_WIDE", 1)
 // power (dH and dW tiles compete for L2 at the transition), lowering clocks
 // for the whole step (-2.3% tokens/s, profiles/r1/SUMMARY.md).
 static bool fused_bwd() { return wide_bwd() && env_int("RLHEAD_FUSED_BWD", 0) != 0; }
-// The q -> dZ rescale can run inside the dH / dW GEMMs (converter warps of the
-// 512-wide CTA-pair tiles, separate launches).
-bool tc_can_convert_dz() { return wide_bwd() && !fused_bwd(); }
 template <int AMN, int BMN, int EPI>
 static rl_status run_wide(const CUtensorMap& a, const CUtensorMap& b, TcArgs t, int64_t m_extent,
                           int kind, cudaStream_t s, const CUtensorMap* a2 = nullptr,
@@ -1154,7 +1013,7 @@ rl_status launch_tc_fwd(const rl_head* hd, const void* weight, const WsLayout& L
 rl_status launch_tc_bwd(const rl_head* hd, const void* weight, void* grad_hidden,
                         float* grad_hidden_f32, bool gh_multicast, float* grad_weight,
                         const rl_peer_group* dw_rs, bool entropy_on, const WsLayout& L, char* ws,
-                        cudaStream_t s, bool dz_ready, int bwd_rows, bool dz_convert) {
+                        cudaStream_t s, bool dz_ready, int bwd_rows) {
   const int h = hd->hidden, V = hd->vocab;
   const int cg = tc_cta_group();
   const bool packed = bwd_rows == BWD_PACKED;
@@ -1241,20 +1100,7 @@ rl_status launch_tc_bwd(const rl_head* hd, const void* weight, void* grad_hidden
     t7.rs_rows = dw_rs->rows_per_rank;
     for (int q = 0; q < dw_rs->world; ++q) t7.rs_peer[q] = dw_rs->peers[q];
   }
-  if (dz_convert) {
-    // fused q -> dZ inside the dH / dW launches (converter warps; the prefix
-    // row layout keeps q and the per-row state at the same compact index)
-    if (bwd_rows != BWD_PREFIX || !tc_can_convert_dz()) return RL_ERR_INVALID_ARG;
-    for (TcArgs* t : {&t6, &t7}) {
-      t->cvt = 1;
-      t->cv_pm = reinterpret_cast<const float*>(ws + L.off_pm);
-      t->cv_zy = reinterpret_cast<const float*>(ws + L.off_zy);
-      t->cv_nvt = L.n_vt;
-      t->lse_c = reinterpret_cast<const float*>(ws + L.off_lse);
-      t->g_c = reinterpret_cast<const float*>(ws + L.off_g);
-    }
-  }
-  if (fused_bwd() && !dz_convert) {
+  if (fused_bwd()) {
     // one persistent launch over the dH tiles then the dW tiles: the last
     // (partial) wave of dH fills with dW tiles instead of idling.
     TcArgs t = t6;
@@ -1299,7 +1145,6 @@ rl_status launch_tc_bwd(const rl_head* hd, const void* weight, void* grad_hidden
   // launch runs 256-wide tiles (two accumulators: the next tile's MMA overlaps
   // the stores). RLHEAD_RS_NARROW=0 keeps the 512-wide tiles.
   const bool rs_narrow = t7.rs_world > 0 && env_int("RLHEAD_RS_NARROW", 1) != 0;
-  if (rs_narrow && t7.cvt) return RL_ERR_INVALID_ARG;
   return run_wide<1, 1, EPI_ACC>(ma7, mb7, t7, V, RL_K_GEMM_DW, s,
                                  t7.acc_red == 2 ? &macc : nullptr, rs_narrow);
 }

@@ -168,15 +168,10 @@ def test_backward_row_skip(rl):
         gh_d, gw_d = _env_run(rl, {"RLHEAD_BWD_SKIP": "0", "RLHEAD_DZ_FUSED": "0"}, run)
         # A != 0 rows moved ahead of the A = 0 rows before the forward (fused mode)
         gh_f, gw_f = _env_run(rl, {"RLHEAD_BWD_SKIP": "1", "RLHEAD_DZ_FUSED": "1"}, run)
-        # ... and q rescaled into dZ inside the dH / dW GEMMs (converter warps)
-        gh_c, gw_c = _env_run(rl, {"RLHEAD_BWD_SKIP": "1", "RLHEAD_DZ_FUSED": "2"}, run)
         assert torch.equal(gh_s, gh_d), kl
         assert torch.equal(gh_f, gh_d), kl
-        assert torch.equal(gh_c, gh_d), kl
         assert float((gw_s - gw_d).norm() / gw_d.norm()) <= 1e-5, kl
         assert float((gw_f - gw_d).norm() / gw_d.norm()) <= 1e-5, kl
-        assert float((gw_c - gw_d).norm() / gw_d.norm()) <= 1e-5, kl
-        assert torch.equal(gw_c, gw_f), kl   # same dZ bits, same GEMM order
         ref = oracle.policy_loss_fwd_bwd(H, W, lay.cu_seqlens, lay.mask, lay.targets, old, adv,
                                          oracle.LossParams(kl_coef=kl), n_global=lay.num_tokens,
                                          ref_logp=ref_lp.astype(np.float64))

@@ -32,16 +32,13 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
                                   "RLHEAD_DYN_SCHED": "1"},
                                  {"RLHEAD_DZ_RECOMPUTE": "1"},
                                  {"RLHEAD_DZ_RECOMPUTE": "1", "RLHEAD_FUSED_BWD": "1"},
-                                 {"RLHEAD_DZ_FUSED": "1"},
-                                 {"RLHEAD_DZ_FUSED": "2"},
-                                 {"RLHEAD_DZ_FUSED": "2", "RLHEAD_DYN_SCHED": "0"}],
+                                 {"RLHEAD_DZ_FUSED": "1"}],
                          ids=["cta1", "cta2-narrow", "cta2-wide-fused", "cta2-unfused-raster",
                               "dw-load-store", "dw-red-fused", "dw-tma-reduce", "l2-hints",
                               "dw-serpentine", "non-persistent",
                               "dyn-sched", "dyn-sched-fused", "dyn-sched-cta1",
                               "dz-tma-cta1", "tma-all-dyn", "dz-recompute",
-                              "dz-recompute-fused", "dz-fused-prefix", "dz-in-gemm",
-                              "dz-in-gemm-static"])
+                              "dz-recompute-fused", "dz-fused-prefix"])
 def test_variant_parity(env):
     import torch
     if not torch.cuda.is_available():

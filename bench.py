@@ -61,9 +61,9 @@ def parse():
                    help="N>1 dW reduction: reduce-scatter fused into the last dW GEMM epilogue "
                         "+ NVLink all-gather (symm), or NCCL all-reduce")
     p.add_argument("--dw-output", default="full", choices=["full", "shard"],
-                   help="N>1 with symm: every rank ends with the whole reduced dW (full), or "
-                        "only its owned rows (shard: FSDP / ZeRO-2 gradient reduce-scatter, "
-                        "no broadcast)")
+                   help="N>1: every rank ends with the whole reduced dW (full), or only its "
+                        "owned rows (shard: FSDP / ZeRO-2 gradient reduce-scatter, no "
+                        "broadcast / all-gather)")
     p.add_argument("--split-groups", type=int, default=0,
                    help="N>1: LPT over single sequences (group statistics all-reduced) "
                         "instead of whole groups -- finer balance for few large groups")
@@ -351,12 +351,13 @@ def main():
         step = PolicyLossStep(head, W, db, group=group,
                               collective="symm" if collective == "symm" else "nccl",
                               pipeline=bool(args.pipeline), split_groups=split,
-                              dw_output=args.dw_output if collective == "symm" else "full")
+                              dw_output=args.dw_output if world > 1 else "full")
     except Exception as e:  # symmetric memory unavailable: NCCL all-reduce instead
         print(f"[bench] collective=symm unavailable ({e}); using nccl", file=sys.stderr)
         collective = "nccl"
         step = PolicyLossStep(head, W, db, group=group, collective="nccl",
-                              pipeline=bool(args.pipeline), split_groups=split)
+                              pipeline=bool(args.pipeline), split_groups=split,
+                              dw_output=args.dw_output if world > 1 else "full")
     gh = torch.empty(max_mb, cfg.hidden, dtype=H.dtype, device=dev)
     tokens_local = int(sum(int(mine.mask[r0:r1].sum()) for _, _, r0, r1, _ in db.mbs))
     tok_t = torch.tensor([tokens_local], dtype=torch.int64, device=dev)
@@ -415,9 +416,13 @@ def main():
         keys = ["zero_dw", "count_allreduce", "advantage", "micro_batches", "dw_reduce",
                 "stats_gather"]
         t = torch.tensor([ph.get(k, 0.0) for k in keys], dtype=torch.float64, device=dev)
+        t_min = t.clone()
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dist.all_reduce(t_min, op=dist.ReduceOp.MIN)
         phases = {k: round(float(v), 3) for k, v in zip(keys, t.tolist())}
+        if world > 1:   # max - min of a phase: the slowest rank's lead (imbalance / waiting)
+            phases["min_over_ranks"] = {k: round(float(v), 3) for k, v in zip(keys, t_min.tolist())}
         phases["note"] = "one extra untimed step, ms per phase, max over ranks"
 
     # roofline of the dominant kernel (GEMM kinds: 2hV flops per token per launch)
@@ -505,8 +510,7 @@ def main():
                        "global_batch_tokens": tokens_global, "micro_batch_rows": args.mb_rows,
                        "micro_batches_per_rank": len(db.mbs), "parallelism": f"dp{world}",
                        "dw_collective": collective, "pipeline": bool(args.pipeline),
-                       "dw_output": (args.dw_output if collective == "symm" else
-                                     ("full" if world > 1 else "local")),
+                       "dw_output": args.dw_output if world > 1 else "local",
                        "sharding": "sequences (split groups)" if split else "whole groups",
                        "l2": "inputs > L2 (hidden rows of the mini-batch ~ "
                              f"{mine.num_rows * cfg.hidden * 2 / 1e9:.1f} GB per rank)",

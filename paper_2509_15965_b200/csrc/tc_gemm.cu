@@ -928,11 +928,10 @@ static bool wide_bwd() { return tc_cta_group() == 2 && env_int("RLHEAD_WIDE", 1)
 static bool fused_bwd() { return wide_bwd() && env_int("RLHEAD_FUSED_BWD", 0) != 0; }
 template <int AMN, int BMN, int EPI>
 static rl_status run_wide(const CUtensorMap& a, const CUtensorMap& b, TcArgs t, int64_t m_extent,
-                          int kind, cudaStream_t s, const CUtensorMap* a2 = nullptr,
-                          bool force_narrow = false) {
+                          int kind, cudaStream_t s, const CUtensorMap* a2 = nullptr) {
   t.group_m = env_int("RLHEAD_GROUP_M_BWD", 1);
   if (t.group_m < 1) t.group_m = 1;
-  if (wide_bwd() && !force_narrow) {
+  if (wide_bwd()) {
     t.n_tiles = static_cast<int32_t>(ceil_div(t.N, 2 * TC_BN));
     const bool persistent =
         env_int(EPI == EPI_ACC ? "RLHEAD_NONPERSIST_DW" : "RLHEAD_NONPERSIST_DH", 0) == 0;
@@ -1140,13 +1139,8 @@ rl_status launch_tc_bwd(const rl_head* hd, const void* weight, void* grad_hidden
     else if (!make_map_f32(&macc, grad_weight, h, V, static_cast<uint64_t>(h) * 4, 32, 32))
       return RL_ERR_CUDA;
   }
-  // With the reduce-scatter the epilogue stores every tile over NVLink; the
-  // 512-wide tile's single TMEM accumulator would hold the MMA for it, so that
-  // launch runs 256-wide tiles (two accumulators: the next tile's MMA overlaps
-  // the stores). RLHEAD_RS_NARROW=0 keeps the 512-wide tiles.
-  const bool rs_narrow = t7.rs_world > 0 && env_int("RLHEAD_RS_NARROW", 1) != 0;
   return run_wide<1, 1, EPI_ACC>(ma7, mb7, t7, V, RL_K_GEMM_DW, s,
-                                 t7.acc_red == 2 ? &macc : nullptr, rs_narrow);
+                                 t7.acc_red == 2 ? &macc : nullptr);
 }
 
 }  // namespace rlh

@@ -263,10 +263,10 @@ class PolicyLossStep:
         self.R = R
         if dw_output not in ("full", "shard"):
             raise ValueError(f"unknown dw_output {dw_output!r}")
-        if dw_output == "shard" and collective != "symm":
-            raise ValueError("dw_output='shard' needs collective='symm'")
         # "shard": after run(), grad_w_shard (rows shard_rows(V, world, rank))
         # holds this rank's slab of the reduced dW and no broadcast runs
+        # (symm: the fused reduce-scatter's owner sum only; nccl: one
+        # reduce_scatter over the dW rows padded to world x ceil(V / world))
         self.dw_output = dw_output
         if advantage not in ("grpo", "reinforce_pp"):
             raise ValueError(f"unknown advantage {advantage!r}")
@@ -286,15 +286,26 @@ class PolicyLossStep:
         self.params.n_seqs_global = self.n_seqs
         self.adv = torch.empty(max(db.cu.shape[0] - 1, 1), dtype=torch.float32, device=dev)
         self.symm = None
-        if collective == "symm" and _world(group) > 1:
+        P = _world(group)
+        rank = 0
+        if P > 1:
+            import torch.distributed as dist
+            rank = dist.get_rank(group)
+        V, h = weight.shape
+        self._gw_pad = None
+        if collective == "symm" and P > 1:
             self.grad_w, self.staging, self.peer_group, self.out_peers, self.symm = \
                 _symm_dw_buffers(R, weight, group)
+        elif dw_output == "shard" and P > 1:
+            # rows padded to P x ceil(V / P) so reduce_scatter's chunks are equal
+            self._gw_pad = torch.zeros(P * -(-V // P), h, dtype=torch.float32, device=dev)
+            self.grad_w = self._gw_pad[:V]
         else:
-            self.grad_w = torch.zeros(weight.shape[0], weight.shape[1], dtype=torch.float32,
-                                      device=dev)
-        r0, r1 = shard_rows(weight.shape[0], _world(group) if self.symm is not None else 1,
-                            self.peer_group.rank if self.symm is not None else 0)
+            self.grad_w = torch.zeros(V, h, dtype=torch.float32, device=dev)
+        r0, r1 = shard_rows(V, P, rank)
         self.grad_w_shard = self.grad_w[r0:r1]
+        if self._gw_pad is not None:
+            self._shard_out = torch.empty(-(-V // P), h, dtype=torch.float32, device=dev)
         self.stats = R.new_stats(dev)
         self.stats_local = R.new_stats(dev)
         self.logp = torch.empty(max(db.num_rows, 1), dtype=torch.float32, device=dev)
@@ -382,6 +393,10 @@ class PolicyLossStep:
         if self.symm is not None:
             _symm_dw_finish(R, self.symm, self.staging, self.grad_w, self.peer_group,
                             self.out_peers, shard=self.dw_output == "shard")
+        elif self._gw_pad is not None:
+            import torch.distributed as dist
+            dist.reduce_scatter_tensor(self._shard_out, self._gw_pad, group=self.group)
+            self.grad_w_shard.copy_(self._shard_out[:self.grad_w_shard.shape[0]])
         else:
             all_reduce_(self.grad_w, "sum", self.group)
         tm.record("dw_reduce")

@@ -197,8 +197,8 @@ def test_shard_work_weighted():
 
 
 def test_shard_rows_and_dw_output_args():
-    """dw_output="shard" (FSDP / ZeRO-2 gradient: owned rows only) needs the
-    symmetric-memory reduce-scatter; the owned rows follow the header's
+    """dw_output="shard" (FSDP / ZeRO-2 gradient: owned rows only): the owned
+    rows follow the header's
     owner(j) = min(j / ceil(V / P), P - 1) rule and tile [0, V)."""
     from paper_2509_15965_b200.dp import PolicyLossStep, shard_rows
     for V, P in ((152064, 4), (32064, 3), (10, 4), (7, 8)):
@@ -208,7 +208,5 @@ def test_shard_rows_and_dw_output_args():
         rows = -(-V // P)
         for q, (r0, r1) in enumerate(spans):
             assert all(min(j // rows, P - 1) == q for j in range(r0, r1, max(1, (r1 - r0) // 7)))
-    with pytest.raises(ValueError):
-        PolicyLossStep(None, None, None, collective="nccl", dw_output="shard")
     with pytest.raises(ValueError):
         PolicyLossStep(None, None, None, dw_output="bogus")

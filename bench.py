@@ -57,9 +57,10 @@ def parse():
                    help="masked tokens of the cpu_baseline leg (about 10-30 s of oracle work)")
     p.add_argument("--cpu-1t-tokens", type=int, default=64,
                    help="masked tokens of the cpu_baseline leg's 1-thread run (SURVEY M.7)")
-    p.add_argument("--collective", default="symm", choices=["symm", "nccl"],
+    p.add_argument("--collective", default="symm", choices=["symm", "nvls", "nccl"],
                    help="N>1 dW reduction: reduce-scatter fused into the last dW GEMM epilogue "
-                        "+ NVLink all-gather (symm), or NCCL all-reduce")
+                        "+ NVLink all-gather (symm); NVLS in-switch sum after the last dW GEMM "
+                        "(nvls); or NCCL all-reduce / reduce-scatter (nccl)")
     p.add_argument("--dw-output", default="full", choices=["full", "shard"],
                    help="N>1: every rank ends with the whole reduced dW (full), or only its "
                         "owned rows (shard: FSDP / ZeRO-2 gradient reduce-scatter, no "
@@ -349,11 +350,12 @@ def main():
     collective = args.collective if world > 1 else "none"
     try:
         step = PolicyLossStep(head, W, db, group=group,
-                              collective="symm" if collective == "symm" else "nccl",
+                              collective=collective if collective in ("symm", "nvls")
+                              else "nccl",
                               pipeline=bool(args.pipeline), split_groups=split,
                               dw_output=args.dw_output if world > 1 else "full")
     except Exception as e:  # symmetric memory unavailable: NCCL all-reduce instead
-        print(f"[bench] collective=symm unavailable ({e}); using nccl", file=sys.stderr)
+        print(f"[bench] collective={collective} unavailable ({e}); using nccl", file=sys.stderr)
         collective = "nccl"
         step = PolicyLossStep(head, W, db, group=group, collective="nccl",
                               pipeline=bool(args.pipeline), split_groups=split,

@@ -420,6 +420,27 @@ RL_API rl_status rl_reduce_bcast_rows_f32(const float *staging, float *const *ou
                                           float *out_mc, int32_t rank, int32_t world,
                                           int64_t num_rows, int64_t cols, int64_t rows_per_rank,
                                           rl_stream_t stream);
+/* DP dW SUM after the last micro-batch's dW GEMM, without staging (C3 of SURVEY
+ * §8(e), collective "nvls"). Every rank's [num_rows][cols] fp32
+ * dW lives in a buffer that all ranks have mapped: peer_ptrs[q] (HOST array of
+ * world device pointers, peer_ptrs[rank] = the local one). Rank `rank` owns
+ * rows [rank*rows_per_rank, min((rank+1)*rows_per_rank, num_rows)) (the
+ * owner(j) rule of rl_peer_group) and sums them over the ranks:
+ *   mc_ptr != NULL: multimem.ld_reduce.add through the NVLS multicast address
+ *     of the buffer (the switch adds the world copies; its rounding order);
+ *   mc_ptr == NULL: loads from every peer in rank order 0..world-1
+ *     (deterministic).
+ * broadcast != 0: the sum is stored into every rank's buffer (multimem.st, or
+ * P2P stores) -- every rank ends with the whole reduced dW. broadcast == 0:
+ * only into this rank's own buffer (a sharded gradient as FSDP / ZeRO-2
+ * reduce-scatter leaves it; the other rows keep this rank's own partial).
+ * Bracket with cross-rank barriers (all dW GEMMs done before; all sums stored
+ * after). cols % 4 == 0, 16-B aligned pointers, 1 <= world <= 8, else
+ * RL_ERR_INVALID_ARG. */
+RL_API rl_status rl_dw_reduce_rows_f32(float *const *peer_ptrs, float *mc_ptr, int32_t rank,
+                                       int32_t world, int64_t num_rows, int64_t cols,
+                                       int64_t rows_per_rank, int32_t broadcast,
+                                       rl_stream_t stream);
 
 /* dst[t][0:hidden] (bf16, row stride ld) = round-to-nearest(src[t][0:hidden])
  * (fp32, row stride hidden), t < num_rows; hidden even, ld >= hidden even. */

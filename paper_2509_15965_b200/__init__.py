@@ -11,7 +11,7 @@ from .rlhead import (  # noqa: F401
     rl_launch_count, rl_logprob_fwd, rl_policy_loss_fwd_bwd, rl_workspace_size,
     rl_logprob_partials, rl_logprob_merge, rl_policy_loss_fwd_bwd_vp,
     rl_minibatch_early_stop, rl_scale_by_inverse_count, rl_gae, rl_value_loss_fwd_bwd,
-    rl_allreduce_sum_f32, rl_reduce_bcast_rows_f32, rl_cast_rows_bf16, rl_batch_norm_advantage,
+    rl_allreduce_sum_f32, rl_reduce_bcast_rows_f32, rl_dw_reduce_rows_f32, rl_cast_rows_bf16, rl_batch_norm_advantage,
     rl_read_device_error, rl_loss_stats_reduce, rl_policy_loss_fwd, rl_policy_loss_bwd,
     RL_DEVERR_CU_SEQLENS, RL_DEVERR_GROUP, RL_DEVERR_TARGET, KERNEL_KINDS, EXPORTED,
 )

@@ -62,6 +62,79 @@ k_p2p_allreduce_f32(PeerPtrs peers, int64_t n4, int rank, int world) {
   }
 }
 
+// DP dW sum after the last dW GEMM (collective "nvls"): rank r
+// owns float4s [b4, e4) of the [rows][cols] buffer. NVLS: multimem.ld_reduce
+// pulls the element-wise sum of every rank's copy through the switch; the sum
+// goes back to every copy (multimem.st, bcast = 1) or into this rank's own
+// buffer only (bcast = 0: a sharded gradient). P2P: loads from every peer in
+// rank order (deterministic), stores to every peer or to this rank only.
+// RD_UNROLL independent loads per thread keep the NVLink requests in flight.
+constexpr int RD_UNROLL = 4;
+__global__ void __launch_bounds__(AR_THREADS)
+k_nvls_rows_reduce_f32(float* mc, float* local, int64_t b4, int64_t e4, int bcast) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * AR_THREADS;
+  for (int64_t i0 = b4 + static_cast<int64_t>(blockIdx.x) * AR_THREADS + threadIdx.x; i0 < e4;
+       i0 += stride * RD_UNROLL) {
+    uint32_t v[RD_UNROLL][4];
+#pragma unroll
+    for (int u = 0; u < RD_UNROLL; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i < e4)
+        asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(v[u][0]), "=r"(v[u][1]), "=r"(v[u][2]), "=r"(v[u][3])
+                     : "l"(mc + 4 * i)
+                     : "memory");
+    }
+#pragma unroll
+    for (int u = 0; u < RD_UNROLL; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i >= e4) continue;
+      if (bcast)
+        asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(mc + 4 * i),
+                     "r"(v[u][0]), "r"(v[u][1]), "r"(v[u][2]), "r"(v[u][3])
+                     : "memory");
+      else
+        reinterpret_cast<uint4*>(local)[i] = make_uint4(v[u][0], v[u][1], v[u][2], v[u][3]);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(AR_THREADS)
+k_p2p_rows_reduce_f32(PeerPtrs peers, int64_t b4, int64_t e4, int rank, int world, int bcast) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * AR_THREADS;
+  for (int64_t i0 = b4 + static_cast<int64_t>(blockIdx.x) * AR_THREADS + threadIdx.x; i0 < e4;
+       i0 += stride * RD_UNROLL) {
+    float4 s[RD_UNROLL];
+#pragma unroll
+    for (int u = 0; u < RD_UNROLL; ++u) {
+      const int64_t i = i0 + u * stride;
+      s[u] = i < e4 ? reinterpret_cast<const float4*>(peers.p[0])[i] : make_float4(0, 0, 0, 0);
+    }
+    for (int q = 1; q < world; ++q) {  // fixed rank order: deterministic
+#pragma unroll
+      for (int u = 0; u < RD_UNROLL; ++u) {
+        const int64_t i = i0 + u * stride;
+        if (i >= e4) continue;
+        const float4 x = reinterpret_cast<const float4*>(peers.p[q])[i];
+        s[u].x += x.x;
+        s[u].y += x.y;
+        s[u].z += x.z;
+        s[u].w += x.w;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < RD_UNROLL; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i >= e4) continue;
+      if (bcast) {
+        for (int q = 0; q < world; ++q) reinterpret_cast<float4*>(peers.p[q])[i] = s[u];
+      } else {
+        reinterpret_cast<float4*>(peers.p[rank])[i] = s[u];
+      }
+    }
+  }
+}
+
 // Owner side of the DP dW reduce-scatter: sum the `world`
 // staged copies of this rank's slab in rank order (deterministic) and store
 // the sum into every rank's output -- multimem.st through the multicast
@@ -166,6 +239,39 @@ rl_status rl_reduce_bcast_rows_f32(const float* staging, float* const* out_peers
   TraceScope ts(RL_K_MISC, s);
   k_reduce_bcast_f32<<<blocks, AR_THREADS, 0, s>>>(staging, rows_per_rank * cols / 4, world, pp,
                                                    out_mc, r0 * cols / 4, n4);
+  RLH_CHECK_LAUNCH();
+  return RL_OK;
+}
+
+rl_status rl_dw_reduce_rows_f32(float* const* peer_ptrs, float* mc_ptr, int32_t rank,
+                                int32_t world, int64_t num_rows, int64_t cols,
+                                int64_t rows_per_rank, int32_t broadcast, rl_stream_t stream) {
+  if (world < 1 || world > AR_MAX_PEERS || rank < 0 || rank >= world || num_rows < 0 ||
+      cols <= 0 || (cols & 3) || rows_per_rank <= 0 || rows_per_rank * world < num_rows ||
+      !peer_ptrs)
+    return RL_ERR_INVALID_ARG;
+  PeerPtrs pp{};
+  for (int q = 0; q < world; ++q) {
+    if (!peer_ptrs[q] || (reinterpret_cast<uintptr_t>(peer_ptrs[q]) & 15) != 0)
+      return RL_ERR_INVALID_ARG;
+    pp.p[q] = peer_ptrs[q];
+  }
+  if (mc_ptr && (reinterpret_cast<uintptr_t>(mc_ptr) & 15) != 0) return RL_ERR_INVALID_ARG;
+  if (world == 1) return RL_OK;
+  const int64_t r0 = std::min<int64_t>(static_cast<int64_t>(rank) * rows_per_rank, num_rows);
+  const int64_t r1 = std::min(r0 + rows_per_rank, num_rows);
+  if (r1 <= r0) return RL_OK;
+  const int64_t b4 = r0 * cols / 4, e4 = r1 * cols / 4;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int blocks = static_cast<int>(
+      std::min<int64_t>(ceil_div(ceil_div(e4 - b4, RD_UNROLL), AR_THREADS), 148 * 4));
+  TraceScope ts(RL_K_MISC, s);
+  if (mc_ptr)
+    k_nvls_rows_reduce_f32<<<blocks, AR_THREADS, 0, s>>>(mc_ptr, pp.p[rank], b4, e4,
+                                                          broadcast ? 1 : 0);
+  else
+    k_p2p_rows_reduce_f32<<<blocks, AR_THREADS, 0, s>>>(pp, b4, e4, rank, world,
+                                                         broadcast ? 1 : 0);
   RLH_CHECK_LAUNCH();
   return RL_OK;
 }

@@ -270,7 +270,7 @@ class PolicyLossStep:
         self.dw_output = dw_output
         if advantage not in ("grpo", "reinforce_pp"):
             raise ValueError(f"unknown advantage {advantage!r}")
-        if collective not in ("nccl", "symm"):
+        if collective not in ("nccl", "symm", "nvls"):
             raise ValueError(f"unknown collective {collective!r}")
         self.advantage = advantage
         self.split_groups = split_groups
@@ -293,9 +293,18 @@ class PolicyLossStep:
             rank = dist.get_rank(group)
         V, h = weight.shape
         self._gw_pad = None
+        self.nvls = None
         if collective == "symm" and P > 1:
             self.grad_w, self.staging, self.peer_group, self.out_peers, self.symm = \
                 _symm_dw_buffers(R, weight, group)
+        elif collective == "nvls" and P > 1:
+            # dW in symmetric memory, summed after the last dW GEMM by
+            # rl_dw_reduce_rows_f32 (NVLS in-switch reduce; P2P without NVLS)
+            import torch.distributed._symmetric_memory as symm_mem
+            import torch.distributed as dist
+            t = symm_mem.empty(V * h, dtype=torch.float32, device=dev)
+            self.nvls = symm_mem.rendezvous(t, group if group is not None else dist.group.WORLD)
+            self.grad_w = t.view(V, h)
         elif dw_output == "shard" and P > 1:
             # rows padded to P x ceil(V / P) so reduce_scatter's chunks are equal
             self._gw_pad = torch.zeros(P * -(-V // P), h, dtype=torch.float32, device=dev)
@@ -393,6 +402,14 @@ class PolicyLossStep:
         if self.symm is not None:
             _symm_dw_finish(R, self.symm, self.staging, self.grad_w, self.peer_group,
                             self.out_peers, shard=self.dw_output == "shard")
+        elif self.nvls is not None:
+            hdl = self.nvls
+            hdl.barrier(channel=0)      # every rank's dW GEMMs done
+            R.rl_dw_reduce_rows_f32(self.grad_w, hdl.rank, hdl.world_size,
+                                    -(-self.grad_w.shape[0] // hdl.world_size),
+                                    list(hdl.buffer_ptrs), mc_ptr=hdl.multicast_ptr or 0,
+                                    broadcast=self.dw_output == "full")
+            hdl.barrier(channel=0)      # every owned slab summed (and broadcast)
         elif self._gw_pad is not None:
             import torch.distributed as dist
             dist.reduce_scatter_tensor(self._shard_out, self._gw_pad, group=self.group)

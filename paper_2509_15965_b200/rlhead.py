@@ -108,6 +108,9 @@ lib.rl_allreduce_sum_f32.argtypes = [C.POINTER(C.c_void_p), _vp, C.c_int32, C.c_
 lib.rl_reduce_bcast_rows_f32.restype = C.c_int
 lib.rl_reduce_bcast_rows_f32.argtypes = [_vp, C.POINTER(C.c_void_p), _vp, C.c_int32, C.c_int32,
                                          C.c_int64, C.c_int64, C.c_int64, _vp]
+lib.rl_dw_reduce_rows_f32.restype = C.c_int
+lib.rl_dw_reduce_rows_f32.argtypes = [C.POINTER(C.c_void_p), _vp, C.c_int32, C.c_int32,
+                                      C.c_int64, C.c_int64, C.c_int64, C.c_int32, _vp]
 lib.rl_cast_rows_bf16.restype = C.c_int
 lib.rl_cast_rows_bf16.argtypes = [_vp, C.c_int64, C.c_int32, _vp, C.c_int64, _vp]
 lib.rl_minibatch_early_stop.restype = C.c_int
@@ -143,7 +146,7 @@ EXPORTED = ["rl_workspace_size", "rl_batch_prepare", "rl_logprob_fwd", "rl_grpo_
             "rl_value_workspace_size", "rl_value_loss_fwd_bwd", "rl_allreduce_sum_f32",
             "rl_cast_rows_bf16", "rl_batch_norm_advantage", "rl_read_device_error",
             "rl_reduce_bcast_rows_f32", "rl_loss_stats_reduce", "rl_policy_loss_fwd",
-            "rl_policy_loss_bwd"]
+            "rl_policy_loss_bwd", "rl_dw_reduce_rows_f32"]
 
 
 class RLHeadError(RuntimeError):
@@ -462,6 +465,20 @@ def rl_reduce_bcast_rows_f32(staging, out, rank: int, world: int, rows_per_rank:
                                         C.c_void_p(int(mc_ptr)) if mc_ptr else None, int(rank),
                                         int(world), int(rows), int(cols), int(rows_per_rank),
                                         _stream(stream)), "rl_reduce_bcast_rows_f32")
+
+
+def rl_dw_reduce_rows_f32(out, rank: int, world: int, rows_per_rank: int, peer_ptrs,
+                          mc_ptr: int = 0, broadcast: bool = True, stream=None):
+    """DP dW sum after the last dW GEMM (no staging): this rank's owned rows of
+    out [rows, cols] (mapped by every rank: peer_ptrs) summed over the ranks --
+    through the NVLS multicast address when mc_ptr, else P2P in rank order --
+    and stored into every rank's copy (broadcast) or this rank's only."""
+    rows, cols = out.shape
+    arr = (C.c_void_p * world)(*[int(x) for x in peer_ptrs])
+    _check(lib.rl_dw_reduce_rows_f32(arr, C.c_void_p(int(mc_ptr)) if mc_ptr else None,
+                                     int(rank), int(world), int(rows), int(cols),
+                                     int(rows_per_rank), 1 if broadcast else 0, _stream(stream)),
+           "rl_dw_reduce_rows_f32")
 
 
 def rl_cast_rows_bf16(src, dst, stream=None):

@@ -27,8 +27,8 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--empty-last", action="store_true")
     ap.add_argument("--modes", default="nccl,symm",
-                    help="comma list of nccl|symm|shard[-split] | stream-nccl|stream-symm[-nolast]; "
-                         "shard = symm without the broadcast (owned dW rows only); "
+                    help="comma list of nccl|symm|nvls[:shard][-split] | "
+                         "stream-nccl|stream-symm[-nolast]; :shard = owned dW rows only; "
                          "-split = sequence-level sharding with all-reduced group statistics "
                          "(compare with --max-mb 0); stream-* = StreamingPolicyLoss (deferred "
                          "1/N), -nolast = no last=True feed (partial sent by finish())")
@@ -113,11 +113,10 @@ def main():
         if mode.startswith("stream-"):
             parts = mode.split("-")
             step = Streamed(db, parts[1], "nolast" not in parts)
-        elif mode.startswith("shard"):   # symm reduce-scatter, no broadcast (FSDP gradient)
-            step = PolicyLossStep(head, W, db, collective="symm", split_groups=split,
-                                  dw_output="shard")
-        else:
-            step = PolicyLossStep(head, W, db, collective=mode.split("-")[0], split_groups=split)
+        else:   # <collective>[:shard]: shard = owned dW rows only (FSDP gradient)
+            coll, _, out_kind = mode.split("-")[0].partition(":")
+            step = PolicyLossStep(head, W, db, collective=coll, split_groups=split,
+                                  dw_output=out_kind or "full")
         step.run(H, old, gh)
         torch.cuda.synchronize()
         dist.barrier()
@@ -131,7 +130,7 @@ def main():
         dist.all_reduce(ms, op=dist.ReduceOp.MAX)
         gws = [torch.empty_like(step.grad_w) for _ in range(world)]
         dist.all_gather(gws, step.grad_w.contiguous())
-        if mode.startswith("shard"):     # rank q's owned rows of its own buffer
+        if ":shard" in mode:             # rank q's owned rows of its own buffer
             full = torch.cat([g[slice(*shard_rows(g.shape[0], world, q))]
                               for q, g in enumerate(gws)])
             res[mode] = (full, rl.read_stats(step.stats), gws)

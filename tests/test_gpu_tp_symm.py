@@ -56,11 +56,14 @@ def test_dp2_fused_dw_reduce_scatter(empty_last):
     # 2 x 32k rows: several whole groups per rank (the first two groups of the
     # generator are forced all-correct / all-wrong, A = 0)
     res = _dp_check(["--config", "qwen1.5b", "--max-mb", "2", "--mb-rows", "32768", "--reps", "1",
-                     "--modes", "nccl,symm,shard"] + (["--empty-last"] if empty_last else []))
+                     "--modes", "nccl,symm,symm:shard,nvls,nvls:shard,nccl:shard"]
+                    + (["--empty-last"] if empty_last else []))
     m = res["modes"]
     assert res["norm_dW"] > 0 and m["symm"]["rel_dW_vs_nccl"] <= 1e-6, res
-    # dw_output="shard": each rank's owned rows are the same sums, no broadcast
-    assert m["shard"]["rel_dW_vs_nccl"] <= 1e-6, res
+    # dw_output="shard": each rank's owned rows are the same sums, no broadcast;
+    # nvls: the sum after the GEMM through the switch (P = 2: two fp32 terms)
+    for k in ("symm:shard", "nvls", "nvls:shard", "nccl:shard"):
+        assert m[k]["rel_dW_vs_nccl"] <= 1e-6, (k, res)
     assert m["symm"]["tokens"] == m["nccl"]["tokens"]
     assert all(v["ranks_identical_dW"] for v in m.values()), res
 

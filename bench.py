@@ -57,7 +57,7 @@ def parse():
                    help="masked tokens of the cpu_baseline leg (about 10-30 s of oracle work)")
     p.add_argument("--cpu-1t-tokens", type=int, default=64,
                    help="masked tokens of the cpu_baseline leg's 1-thread run (SURVEY M.7)")
-    p.add_argument("--collective", default="symm", choices=["symm", "nvls", "nccl"],
+    p.add_argument("--collective", default="nvls", choices=["nvls", "symm", "nccl"],
                    help="N>1 dW reduction: reduce-scatter fused into the last dW GEMM epilogue "
                         "+ NVLink all-gather (symm); NVLS in-switch sum after the last dW GEMM "
                         "(nvls); or NCCL all-reduce / reduce-scatter (nccl)")

@@ -137,6 +137,9 @@ struct TcArgs {
   int32_t acc_red;     // EPI_ACC: 0 load+add+store, 1 red.global.add (L2), 2 TMA reduce-add
                        // of 32x32 smem boxes (tmA2 = fp32 map of acc; 512-wide tiles only)
   int32_t rs_world;    // 0 = off
+  int32_t rs_bulk;     // 512-wide tiles: each lane stages its 128-B row piece in smem and
+                       // ships it with a 1-D bulk copy (whole NVLink lines, asynchronous)
+                       // instead of 16-B stores from registers
   int32_t rs_rank;
   int64_t rs_rows;
   float* rs_peer[8];   // every rank's staging buffer [rs_world][rs_rows][ld_acc]
@@ -677,6 +680,37 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             for (int j = 0; j < 32; ++j) v[j] = 0u;
           }
           if constexpr ((EPI == EPI_ACC || EPI == EPI_BWD) && NB == 2) {
+            if (args.rs_world > 0 && args.rs_bulk) {
+              // (local partial + tile) row piece -> this lane's 128-B line of the
+              // warp's staging buffer (written in rotated chunk order: the 8
+              // lanes of a quarter-warp hit 8 different bank groups), then one
+              // bulk copy per lane into the owner's staging slot over NVLink.
+              // Two buffers per warp: chunk c reuses the one of chunk c - 2.
+              uint8_t* line = smem + C::STG_OFF + ew * 8192 + (c & 1) * 4096 + lane * 128;
+              bulk_wait_group_read<1>();
+              if (row_ok && n0 + c * 32 < args.N) {
+                int64_t own = row / args.rs_rows;
+                own = own < args.rs_world - 1 ? own : args.rs_world - 1;
+                float* slot = args.rs_peer[own] +
+                              (args.rs_rank * args.rs_rows + (row - own * args.rs_rows)) *
+                                  args.ld_acc +
+                              n0 + c * 32;
+#pragma unroll
+                for (int jj = 0; jj < 8; ++jj) {
+                  const int q = (jj + lane) & 7;
+                  float4 o = dst[c * 8 + q];
+                  o.x += __uint_as_float(v[4 * q]);
+                  o.y += __uint_as_float(v[4 * q + 1]);
+                  o.z += __uint_as_float(v[4 * q + 2]);
+                  o.w += __uint_as_float(v[4 * q + 3]);
+                  *reinterpret_cast<float4*>(line + (q << 4)) = o;
+                }
+                fence_proxy_async_smem();
+                bulk_copy_s2g(slot, line, 128);
+                bulk_commit_group();
+              }
+              continue;
+            }
             if (tma_red) {
               // this warp's 32 rows x 32 columns -> a 128-B-swizzled smem box
               // (16-B chunk j of row r at chunk j ^ (r & 7): conflict-free),
@@ -748,6 +782,8 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   }
   if constexpr ((EPI == EPI_ACC || EPI == EPI_BWD) && NB == 2) {
     if (warp >= 4 && lane == 0 && args.acc_red == 2) bulk_wait_group_all();
+    // every lane's bulk copies complete (written at the owner) before exit
+    if (warp >= 4 && args.rs_world > 0 && args.rs_bulk) bulk_wait_group_all();
   }
   if constexpr (EPI == EPI_DZ) {
     if (warp >= 4 && lane == 0 && args.dz_tma) bulk_wait_group_all();
@@ -1098,6 +1134,11 @@ rl_status launch_tc_bwd(const rl_head* hd, const void* weight, void* grad_hidden
     t7.rs_rank = dw_rs->rank;
     t7.rs_rows = dw_rs->rows_per_rank;
     for (int q = 0; q < dw_rs->world; ++q) t7.rs_peer[q] = dw_rs->peers[q];
+    // bulk copies need 16-B aligned rows (ld_acc % 4 == 0, aligned staging)
+    bool al = (t7.ld_acc & 3) == 0;
+    for (int q = 0; q < dw_rs->world; ++q)
+      al = al && (reinterpret_cast<uintptr_t>(dw_rs->peers[q]) & 15) == 0;
+    t7.rs_bulk = al && env_int("RLHEAD_RS_BULK", 0) != 0;
   }
   if (fused_bwd()) {
     // one persistent launch over the dH tiles then the dW tiles: the last

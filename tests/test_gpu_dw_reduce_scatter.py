@@ -34,9 +34,13 @@ def _rank_batches(rl, lay, dev, empty_last):
     return out
 
 
+@pytest.mark.parametrize("bulk", ["0", "1"])
 @pytest.mark.parametrize("empty_last", [False, True])
-def test_fused_dw_reduce_scatter_two_ranks_one_gpu(rl, empty_last):
+def test_fused_dw_reduce_scatter_two_ranks_one_gpu(rl, empty_last, bulk, monkeypatch):
+    """bulk = 1: the epilogue ships each lane's 128-B row piece with a 1-D
+    bulk copy from shared memory (RLHEAD_RS_BULK=1) -- same bits."""
     import torch
+    monkeypatch.setenv("RLHEAD_RS_BULK", bulk)
     dev = "cuda"
     lay = make_layout(CFG, seed=71)
     V, h = CFG.vocab, CFG.hidden

@@ -1138,7 +1138,7 @@ rl_status launch_tc_bwd(const rl_head* hd, const void* weight, void* grad_hidden
     bool al = (t7.ld_acc & 3) == 0;
     for (int q = 0; q < dw_rs->world; ++q)
       al = al && (reinterpret_cast<uintptr_t>(dw_rs->peers[q]) & 15) == 0;
-    t7.rs_bulk = al && env_int("RLHEAD_RS_BULK", 0) != 0;
+    t7.rs_bulk = al && env_int("RLHEAD_RS_BULK", 1) != 0;
   }
   if (fused_bwd()) {
     // one persistent launch over the dH tiles then the dW tiles: the last

@@ -227,6 +227,10 @@ typedef struct rl_peer_group {
   int32_t world;                  /* 1..8                                            */
   int64_t rows_per_rank;          /* > 0, rows_per_rank * world >= vocab             */
   float *peers[8];                /* device: every rank's staging buffer             */
+  int32_t no_partial;             /* 1: grad_weight holds no partial yet (this is the
+                                     rank's only micro-batch of the mini-batch): the
+                                     epilogue sends the tile alone, grad_weight is
+                                     not read. 0: partial + tile                      */
 } rl_peer_group;
 
 /* Loss statistics, device resident, ACCUMULATED (+=) by every call. The

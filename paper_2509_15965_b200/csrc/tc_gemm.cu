@@ -137,6 +137,7 @@ struct TcArgs {
   int32_t acc_red;     // EPI_ACC: 0 load+add+store, 1 red.global.add (L2), 2 TMA reduce-add
                        // of 32x32 smem boxes (tmA2 = fp32 map of acc; 512-wide tiles only)
   int32_t rs_world;    // 0 = off
+  int32_t rs_no_partial;  // acc holds no partial: send the tile alone, do not read acc
   int32_t rs_bulk;     // 512-wide tiles: each lane stages its 128-B row piece in smem and
                        // ships it with a 1-D bulk copy (whole NVLink lines, asynchronous)
                        // instead of 16-B stores from registers
@@ -698,7 +699,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
 #pragma unroll
                 for (int jj = 0; jj < 8; ++jj) {
                   const int q = (jj + lane) & 7;
-                  float4 o = dst[c * 8 + q];
+                  float4 o = args.rs_no_partial ? make_float4(0.f, 0.f, 0.f, 0.f) : dst[c * 8 + q];
                   o.x += __uint_as_float(v[4 * q]);
                   o.y += __uint_as_float(v[4 * q + 1]);
                   o.z += __uint_as_float(v[4 * q + 2]);
@@ -744,7 +745,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                   c * 32);
 #pragma unroll
               for (int q = 0; q < 8; ++q) {
-                float4 o = dst[c * 8 + q];
+                float4 o = args.rs_no_partial ? make_float4(0.f, 0.f, 0.f, 0.f) : dst[c * 8 + q];
                 o.x += __uint_as_float(v[4 * q]);
                 o.y += __uint_as_float(v[4 * q + 1]);
                 o.z += __uint_as_float(v[4 * q + 2]);
@@ -1133,6 +1134,7 @@ rl_status launch_tc_bwd(const rl_head* hd, const void* weight, void* grad_hidden
     t7.rs_world = dw_rs->world;
     t7.rs_rank = dw_rs->rank;
     t7.rs_rows = dw_rs->rows_per_rank;
+    t7.rs_no_partial = dw_rs->no_partial ? 1 : 0;
     for (int q = 0; q < dw_rs->world; ++q) t7.rs_peer[q] = dw_rs->peers[q];
     // bulk copies need 16-B aligned rows (ld_acc % 4 == 0, aligned staging)
     bool al = (t7.ld_acc & 3) == 0;
@@ -1159,6 +1161,7 @@ rl_status launch_tc_bwd(const rl_head* hd, const void* weight, void* grad_hidden
     t.rs_world = t7.rs_world;
     t.rs_rank = t7.rs_rank;
     t.rs_rows = t7.rs_rows;
+    t.rs_no_partial = t7.rs_no_partial;
     for (int q = 0; q < 8; ++q) t.rs_peer[q] = t7.rs_peer[q];
     const int64_t tiles = (ceil_div(L.Rp, 2 * TC_BM) + ceil_div(V, 2 * TC_BM)) * t.n_tiles;
     // dW accumulation as in the separate launch: TMA reduce-add of 32x32

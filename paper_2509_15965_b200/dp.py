@@ -329,6 +329,15 @@ class PolicyLossStep:
             self.ws_pipe = [R.Workspace(dev), R.Workspace(dev)]
             self.aux_stream = torch.cuda.Stream(device=dev)
 
+    def _rs_group(self, last: int):
+        """The fused reduce-scatter's peer group for the last micro-batch; with a
+        single micro-batch grad_w holds no partial yet, so the epilogue need not
+        read it (no_partial)."""
+        if last == 0:
+            import dataclasses
+            return dataclasses.replace(self.peer_group, no_partial=True)
+        return self.peer_group
+
     def count_tokens(self):
         """N = masked tokens (and S = non-empty sequences, for seq-mean
         aggregation) of the whole mini-batch over all ranks."""
@@ -389,8 +398,8 @@ class PolicyLossStep:
             hs = hidden_for_mb(i) if hidden_for_mb else hidden[r0:r1]
             gh = grad_hidden[r0:r1] if full_gh else grad_hidden[:r1 - r0]
             b = R.Batch(cu_mb, self.db.targets[r0:r1], self.db.mask[r0:r1], num_rows=r1 - r0)
-            self.params.dw_reduce_scatter = (self.peer_group if self.symm is not None and i == last
-                                             else None)
+            self.params.dw_reduce_scatter = (self._rs_group(last) if self.symm is not None and
+                                             i == last else None)
             R.rl_policy_loss_fwd_bwd(self.head, hs, self.W, b, old_logp[r0:r1], self.adv[s0:s1],
                                      self.params, self.logp[r0:r1], gh, self.grad_w,
                                      entropy=None if self.entropy is None else self.entropy[r0:r1],
@@ -455,7 +464,7 @@ class PolicyLossStep:
                 after_mb(i)                   # hidden rows are in the workspace now
             with torch.cuda.stream(aux):
                 aux.wait_event(ev_f)
-                self.params.dw_reduce_scatter = (self.peer_group
+                self.params.dw_reduce_scatter = (self._rs_group(last)
                                                  if self.symm is not None and i == last else None)
                 R.rl_policy_loss_bwd(*args, **kw, stream=aux)
                 ev_b[i] = torch.cuda.Event()

@@ -42,7 +42,7 @@ class rl_head(C.Structure):
 
 class rl_peer_group(C.Structure):
     _fields_ = [("rank", C.c_int32), ("world", C.c_int32), ("rows_per_rank", C.c_int64),
-                ("peers", C.c_void_p * 8)]
+                ("peers", C.c_void_p * 8), ("no_partial", C.c_int32)]
 
 
 class rl_loss_params(C.Structure):
@@ -241,10 +241,12 @@ class PeerGroup:
     world: int
     rows_per_rank: int
     peers: list                     # device addresses (ints) of every rank's staging buffer
+    no_partial: bool = False        # grad_weight holds no partial yet (only micro-batch)
 
     def c(self) -> rl_peer_group:
         arr = (C.c_void_p * 8)(*([int(x) for x in self.peers] + [0] * (8 - len(self.peers))))
-        return rl_peer_group(int(self.rank), int(self.world), int(self.rows_per_rank), arr)
+        return rl_peer_group(int(self.rank), int(self.world), int(self.rows_per_rank), arr,
+                             1 if self.no_partial else 0)
 
 
 class Workspace:

@@ -22,6 +22,7 @@ CLASSES = [
     ("UTMALDG", r"UTMALDG"),            # TMA tensor load
     ("UTMASTG", r"UTMASTG"),            # TMA tensor store
     ("UTMAREDG", r"UTMAREDG"),          # TMA tensor reduce (dW += box)
+    ("UBLKCP", r"UBLKCP"),              # 1-D bulk copy (fused reduce-scatter rows to peers)
     ("UTMACCTL.PF", r"UTMACCTL\.PF"),  # TMA descriptor prefetch
     ("LDTM", r"\bLDTM"),                # tcgen05.ld (TMEM -> registers)
     ("UTCATOMSWS", r"UTCATOMSWS"),      # tcgen05.alloc/dealloc

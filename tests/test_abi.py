@@ -53,6 +53,19 @@ def test_workspace_size_and_validation_host_only():
     assert R.lib.rl_status_string(3) == b"RL_ERR_WORKSPACE"
     assert R.lib.rl_grpo_advantage(None, None, -1, 1, None, None, 1e-6, 1, None, None, None) \
         == R.RL_ERR_INVALID_ARG
+    # the DP dW sum (collective "nvls") validates before touching a device pointer
+    peers = (C.c_void_p * 2)(16, 32)
+    dw = R.lib.rl_dw_reduce_rows_f32
+    assert dw(None, None, 0, 2, 10, 8, 5, 1, None) == R.RL_ERR_INVALID_ARG      # no peers
+    assert dw(peers, None, 0, 0, 10, 8, 5, 1, None) == R.RL_ERR_INVALID_ARG     # world 0
+    assert dw(peers, None, 2, 2, 10, 8, 5, 1, None) == R.RL_ERR_INVALID_ARG     # rank >= world
+    assert dw(peers, None, 0, 2, 10, 6, 5, 1, None) == R.RL_ERR_INVALID_ARG     # cols % 4
+    assert dw(peers, None, 0, 2, 11, 8, 5, 1, None) == R.RL_ERR_INVALID_ARG     # 2 x 5 < 11 rows
+    bad = (C.c_void_p * 2)(16, 40)
+    assert dw(bad, None, 0, 2, 10, 8, 5, 1, None) == R.RL_ERR_INVALID_ARG       # misaligned peer
+    assert dw(peers, C.c_void_p(8), 0, 2, 10, 8, 5, 1, None) == R.RL_ERR_INVALID_ARG  # mc align
+    one = (C.c_void_p * 1)(16)
+    assert dw(one, None, 0, 1, 10, 8, 10, 1, None) == R.RL_OK                   # world 1: no-op
 
 
 def test_struct_layouts_match_header(tmp_path):

@@ -968,7 +968,11 @@ static rl_status run_wide(const CUtensorMap& a, const CUtensorMap& b, TcArgs t, 
                           int kind, cudaStream_t s, const CUtensorMap* a2 = nullptr) {
   t.group_m = env_int("RLHEAD_GROUP_M_BWD", 1);
   if (t.group_m < 1) t.group_m = 1;
-  if (wide_bwd()) {
+  // per-GEMM override (A/B of the tile-count quantisation): RLHEAD_WIDE_DH /
+  // RLHEAD_WIDE_DW = 0 runs that GEMM on 256-wide tiles
+  const bool wide =
+      wide_bwd() && env_int(EPI == EPI_ACC ? "RLHEAD_WIDE_DW" : "RLHEAD_WIDE_DH", 1) != 0;
+  if (wide) {
     t.n_tiles = static_cast<int32_t>(ceil_div(t.N, 2 * TC_BN));
     const bool persistent =
         env_int(EPI == EPI_ACC ? "RLHEAD_NONPERSIST_DW" : "RLHEAD_NONPERSIST_DH", 0) == 0;

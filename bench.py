@@ -33,6 +33,10 @@ sys.path.insert(0, ROOT)
 METRIC = "policy-loss fwd+bwd tokens/s at 1/2/4/8 B200; % bf16 tensor-core peak"
 
 
+
+# micro-batch row budget per head, from same-box A/B runs (profiles/r2/SUMMARY.md §3)
+MB_ROWS_DEFAULT = {"qwen1.5b": 32768, "openvla": 32768}
+
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
@@ -40,10 +44,11 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--config", default="qwen7b")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--mb-rows", type=int, default=16384,
-                   help="rows per micro-batch (same-box A/B with the v5 kernels: 32k within "
-                        "0.35%% of 16k but 1.8x the dW DRAM bytes per token, 8k -3.4%%; "
-                        "profiles/r1/SUMMARY.md)")
+    p.add_argument("--mb-rows", type=int, default=None,
+                   help="rows per micro-batch; default per head (MB_ROWS_DEFAULT): 16k for "
+                        "the Qwen-7B/32B heads (same-box: 24k -1.4%%, 32k -2.6%%, 8k -2.6%%), "
+                        "32k for Qwen-1.5B and OpenVLA (h <= 4096 and short steps: +2.0%% / "
+                        "+1.4%% over 16k; profiles/r2/SUMMARY.md)")
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--max-mb", type=int, default=0, help="debug: first micro-batches only")
     p.add_argument("--mb-offset", type=int, default=0,
@@ -74,7 +79,10 @@ def parse():
                    help="per-phase step times (always on for N > 1)")
     p.add_argument("--no-aux", action="store_true",
                    help="skip the auxiliary lines (forward-only path, HBM kernels)")
-    return p.parse_args()
+    a = p.parse_args()
+    if a.mb_rows is None:
+        a.mb_rows = MB_ROWS_DEFAULT.get(a.config, 16384)
+    return a
 
 
 def peaks():

@@ -36,6 +36,9 @@ METRIC = "policy-loss fwd+bwd tokens/s at 1/2/4/8 B200; % bf16 tensor-core peak"
 
 # micro-batch row budget per head, from same-box A/B runs (profiles/r2/SUMMARY.md §3)
 MB_ROWS_DEFAULT = {"qwen1.5b": 32768, "openvla": 32768}
+# sequence-level DP sharding per head (N > 1): OpenVLA's few large groups leave whole-group
+# LPT shards 2.6% apart at 4 GPUs (profiles/r2/r2_vla: +3.1% with split groups)
+SPLIT_GROUPS_DEFAULT = {"openvla": 1}
 
 def parse():
     p = argparse.ArgumentParser()
@@ -70,9 +73,11 @@ def parse():
                    help="N>1: every rank ends with the whole reduced dW (full), or only its "
                         "owned rows (shard: FSDP / ZeRO-2 gradient reduce-scatter, no "
                         "broadcast / all-gather)")
-    p.add_argument("--split-groups", type=int, default=0,
+    p.add_argument("--split-groups", type=int, default=None,
                    help="N>1: LPT over single sequences (group statistics all-reduced) "
-                        "instead of whole groups -- finer balance for few large groups")
+                        "instead of whole groups -- finer balance for few large groups; "
+                        "default per head (SPLIT_GROUPS_DEFAULT: on for OpenVLA, whose 4-GPU "
+                        "whole-group shards differ by 2.6%%)")
     p.add_argument("--pipeline", type=int, default=0,
                    help="1: two-stream micro-batch pipeline (bwd(i) beside fwd(i+1))")
     p.add_argument("--phases", action="store_true",
@@ -82,6 +87,8 @@ def parse():
     a = p.parse_args()
     if a.mb_rows is None:
         a.mb_rows = MB_ROWS_DEFAULT.get(a.config, 16384)
+    if a.split_groups is None:
+        a.split_groups = SPLIT_GROUPS_DEFAULT.get(a.config, 0)
     return a
 
 
